@@ -1,0 +1,156 @@
+/* qspec_b200.h -- C ABI of the B200-native QSpec decode hot path.
+ *
+ * Plain pointers and sizes only: every buffer is caller-allocated device memory,
+ * every call is asynchronous on the caller's cudaStream_t (passed as void*),
+ * nothing allocates or synchronises, and errors come back as status codes
+ * (QS_OK == 0) that the Python shim maps onto the reference exception classes
+ * (pkg/src/qspec/errors.py:6-39).
+ *
+ * Reference interfaces replaced (file:line under /root/reference/pkg/src/qspec):
+ *   qs_quantize_weight / qs_init_weight  <- quant.py:197-218 quantize_groupwise,
+ *                                           storage.py:135-182 random_init (LCG draws)
+ *   qs_lcg_fill                          <- storage.py:62-101 Lcg64.fill
+ *   qs_repack_ref                        <- storage.py:352-422 load_checkpoint (codes+scales)
+ *   qs_act_quant                         <- quant.py:179-194 _quantize_groups,
+ *                                           quant.py:229-245 fake_quantize_activations
+ *   qs_w4a4_linear / qs_w4a16_linear     <- quant.py:248-261 qlinear_forward (LOW / HIGH)
+ *   qs_forward                           <- model.py:255-348 forward
+ *   qs_draft_prep / qs_verify_prep /
+ *   qs_accept / qs_ar_prep / qs_ar_commit <- specdec.py:103-176, 258-335 (+ model.py:211-229 kv_commit)
+ */
+#ifndef QSPEC_B200_H
+#define QSPEC_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  QS_OK = 0,
+  QS_ERR_SHAPE = 1,    /* -> ShapeError */
+  QS_ERR_CONFIG = 2,   /* -> ConfigError */
+  QS_ERR_OVERFLOW = 3, /* -> SequenceOverflowError */
+  QS_ERR_TOKEN = 4,    /* -> TokenIdError */
+  QS_ERR_CUDA = 5      /* CUDA launch / runtime failure */
+};
+
+enum { QS_MODE_HIGH = 0, QS_MODE_LOW = 1 }; /* quant.py:37-41 ExecutionMode */
+
+/* One quantised weight store in the device chunk layout. */
+typedef struct {
+  const uint8_t* codes; /* [n_tiles][n_chunks][4][128][16] packed int4 */
+  const float* scales;  /* [G][n_pad] */
+  int32_t n, k, g, n_pad, n_tiles, G, gp, cpg, n_chunks;
+} qs_qweight_t;
+
+typedef struct {
+  const float* attn_norm;
+  const float* ffn_norm;
+  qs_qweight_t qkv;     /* rows: q | k | v */
+  qs_qweight_t o;
+  qs_qweight_t gate_up; /* rows interleaved: gate_i, up_i */
+  qs_qweight_t down;
+  float* k_cache;       /* [num_pages][n_kv_heads][page][head_dim] fp32 */
+  float* v_cache;
+} qs_layer_t;
+
+typedef struct {
+  int32_t n_layers, d_model, n_heads, n_kv_heads, d_ff, vocab, group_size, rope_len;
+  float norm_eps;
+  const float* tok_emb;    /* [vocab][d_model] */
+  const float* final_norm; /* [d_model] */
+  const float* rope_cos;   /* [rope_len][head_dim/2] */
+  const float* rope_sin;
+  qs_qweight_t lm_head;
+  const qs_layer_t* layers; /* HOST array [n_layers] */
+  const int32_t* block_table; /* device [slots][bt_ld] page ids */
+  int32_t bt_ld, page;
+} qs_model_t;
+
+/* One forward pass: T tokens; query blocks = runs of tokens of one slot. */
+typedef struct {
+  int32_t T;
+  const int32_t* tokens;    /* device [T] */
+  const int32_t* positions; /* device [T] absolute positions */
+  const int32_t* slots;     /* device [T] KV slot (block-table row) */
+  int32_t n_blk;
+  const int32_t* blk_tok0;  /* device [n_blk] */
+  const int32_t* blk_ntok;  /* device [n_blk] */
+  int32_t blk_qmax;         /* max tokens per block (<= 64 / (n_heads/n_kv_heads)) */
+  int32_t ctx_cap;          /* max context any query can see */
+} qs_batch_t;
+
+typedef struct {
+  float* x;       /* [t_max][d_model] residual stream */
+  float* h;       /* [t_max][d_ff] */
+  float* attn;    /* [t_max][d_model] */
+  float* q;       /* [t_max][n_heads*head_dim] */
+  uint8_t* img;   /* activation operand image */
+  float* ascale;  /* activation scales */
+  float* part;    /* stream-K partials */
+  int32_t* counters; /* zero-initialised once; kernels leave them zero */
+  float* arg_val;
+  int32_t* arg_idx;
+} qs_workspace_t;
+
+typedef struct {
+  size_t x, h, attn, q, img, ascale, part, counters, arg_val, arg_idx; /* bytes */
+} qs_workspace_sizes_t;
+
+/* Device sequence state for B slots (SoA), driven by the control kernels. */
+typedef struct {
+  int32_t *pending, *committed, *n_out, *done, *finish, *max_new, *g_eff, *drafted, *out_tokens;
+  int32_t *n_drafted, *n_accepted, *n_cycles, *dropped, *trace, *trace_tok;
+  int32_t out_cap, trace_cap;
+  int32_t B, gamma, eos, max_seq;
+  int32_t *tok, *pos, *slot;
+  const int32_t* argmax;
+} qs_seq_t;
+
+/* ------------------------------------------------------------------ info */
+const char* qs_version(void);
+int qs_num_sms(int32_t* out);
+int qs_linear_max_tokens(void); /* largest T one linear launch accepts (64) */
+int qs_workspace_size(const qs_model_t* m, int32_t t_max, qs_workspace_sizes_t* out);
+int qs_qweight_geometry(int32_t n, int32_t k, int32_t g, qs_qweight_t* out); /* fills dims, not pointers */
+
+/* --------------------------------------------------------------- weights */
+int qs_init_weight(uint64_t seed, uint64_t draw_offset, float scale, int32_t rows, int32_t cols, int32_t g,
+                   uint8_t* codes, float* scales, int32_t n_pad, int32_t row_off, int32_t row_stride,
+                   uint8_t* ref_codes, float* ref_scales, void* stream);
+int qs_quantize_weight(const float* w, int32_t rows, int32_t cols, int32_t g, uint8_t* codes, float* scales,
+                       int32_t n_pad, int32_t row_off, int32_t row_stride, uint8_t* ref_codes, float* ref_scales,
+                       void* stream);
+int qs_lcg_fill(float* out, uint64_t seed, uint64_t draw_offset, int64_t count, float scale, void* stream);
+int qs_repack_ref(const uint8_t* ref_codes, const float* ref_scales, int32_t rows, int32_t cols, int32_t g,
+                  uint8_t* codes, float* scales, int32_t n_pad, int32_t row_off, int32_t row_stride, void* stream);
+
+/* ------------------------------------------------------------- operators */
+int qs_act_quant(const float* x, int32_t T, int32_t K, int32_t g, int8_t* codes, float* scales, float* fq,
+                 void* stream);
+int qs_w4a4_linear(const qs_qweight_t* w, const float* x, int32_t T, float* y, const qs_workspace_t* ws,
+                   void* stream);
+int qs_w4a16_linear(const qs_qweight_t* w, const float* x, int32_t T, float* y, const qs_workspace_t* ws,
+                    void* stream);
+/* raw int32 per-(row, group, image-row) dots of the tensor-core integer core */
+int qs_linear_group_dots(const qs_qweight_t* w, const float* x, int32_t T, int32_t mode, int32_t* dots,
+                         const qs_workspace_t* ws, void* stream);
+
+/* ------------------------------------------------------------------ step */
+int qs_forward(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const qs_workspace_t* ws, float* logits,
+               int32_t* argmax, void* stream);
+
+/* --------------------------------------------------------------- control */
+int qs_draft_prep(const qs_seq_t* s, int32_t step, void* stream);
+int qs_verify_prep(const qs_seq_t* s, void* stream);
+int qs_accept(const qs_seq_t* s, void* stream);
+int qs_ar_prep(const qs_seq_t* s, void* stream);
+int qs_ar_commit(const qs_seq_t* s, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QSPEC_B200_H */

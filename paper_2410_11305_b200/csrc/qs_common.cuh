@@ -1,0 +1,149 @@
+// Shared definitions: device layouts, argument blocks and helpers.
+//
+// Device weight layout ("chunk layout", produced once at load/quantize time):
+//   codes  [n_tiles][n_chunks][4][128][16] bytes
+//          tile  = 128 output rows, chunk = 128 (padded) K positions.
+//          piece j (0..3) of row r holds packed bytes pb = 16j..16j+15 of the
+//          row's 64-byte chunk; packed byte pb = nib(code[k=pb]) | nib(code[k=64+pb]) << 4
+//          (two's-complement nibbles, k relative to the chunk).  Groups of g
+//          codes are zero-padded to gp = roundup(g, 128) so every chunk belongs
+//          to exactly one quantisation group (cpg = gp/128 chunks per group).
+//   scales [G][n_pad] fp32 (group-major so a tile reads one coalesced row).
+// Activation operand image (produced per step by act_pack):
+//   img    [n_chunks][r_pad][128] int8, 128B-swizzled K-major (UMMA SW128),
+//          row = token*L + limb.  L = 1 (W4A4 draft: int4 codes in int8),
+//          L = 3 (W4A16 verify: 24-bit fixed point split in three int8 limbs).
+//   ascale [G][a_ld] fp32 per (group, token): s_x (draft) or 2^-e (verify).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace qs {
+
+constexpr int kTileN = 128;    // output rows per tile (UMMA M)
+constexpr int kChunkK = 128;   // K positions per chunk (one SW128 row of int8)
+constexpr int kChunkBytes = kTileN * kChunkK / 2;  // 8 KiB packed weights per (tile, chunk)
+
+__host__ __device__ inline int ceil_div(int a, int b) { return (a + b - 1) / b; }
+__host__ __device__ inline int round_up(int a, int b) { return ceil_div(a, b) * b; }
+// rows of the activation image for T tokens with L limbs (UMMA N: 8 or 16k)
+__host__ __device__ inline int img_rows(int T, int L) {
+  int r = T * L;
+  return r <= 8 ? 8 : round_up(r, 16);
+}
+
+enum PostOp : int {
+  kOpStore = 0,     // out[t, n] = y
+  kOpResidual = 1,  // out[t, n] += y          (o_proj / down_proj)
+  kOpSiluMul = 2,   // out[t, n/2] = silu(y[2i]) * y[2i+1]   (interleaved gate/up)
+  kOpQkvRope = 3,   // rope(q) -> out, rope(k) -> K cache, v -> V cache
+  kOpLogits = 4,    // logits (optional store) + fused argmax
+  kOpDump = 5,      // debug: raw int32 group dots
+};
+
+struct LinearArgs {
+  const uint8_t* codes;
+  const float* wscale;
+  const uint8_t* act;
+  const float* ascale;
+  int n, n_pad, n_tiles, G, cpg, n_chunks;
+  int T, r_pad, a_ld;
+  int n_cta;
+  float* part;     // [(n_cta + n_tiles)][tmax][128]
+  int* counters;   // [n_tiles + 1], zero on entry, left zero on exit
+  int op;
+  float* out;
+  int ldo;
+  // kOpQkvRope
+  const int* pos;
+  const int* slot;
+  const float* rope_cos;
+  const float* rope_sin;
+  int hd, n_q, n_k, n_kv_heads;
+  float* kcache;
+  float* vcache;
+  const int* block_table;
+  int bt_ld, page;
+  // kOpLogits
+  float* arg_val;
+  int* arg_idx;
+  int* argmax_out;
+  // kOpDump
+  int32_t* dump;
+};
+
+struct PackArgs {
+  const float* x;
+  int ldx;
+  const int* gather_ids;
+  const float* emb;
+  float* x_out;
+  const float* rms_w;
+  float eps;
+  int T, K, g, gp, G, n_chunks, r_pad, a_ld;
+  uint8_t* img;
+  float* ascale;
+  int8_t* codes_out;
+  float* scales_out;
+  float* fq_out;
+  float* y_out;
+};
+
+struct AttnArgs {
+  const float* q;
+  int ldq;
+  const float* kcache;
+  const float* vcache;
+  const int* block_table;
+  int bt_ld, page;
+  const int* pos;
+  const int* slot;
+  const int* blk_tok0;
+  const int* blk_ntok;
+  int H, KV, hd, hpk;
+  float inv_sqrt_hd;
+  int qmax, ctx_cap;
+  float* out;
+  int ldo;
+};
+
+struct QuantWArgs {
+  // source: LCG (src == nullptr) or fp32 row-major [rows, cols]
+  const float* src;
+  unsigned long long seed, offset;  // offset = draw index of element (0, 0)
+  float scale;                      // f32(1/sqrt(d_model)) applied to LCG draws
+  int rows, cols, g;
+  // destination chunk layout
+  uint8_t* codes;
+  float* scales;
+  int n_pad, n_chunks, gp, G;
+  int row_off, row_stride;  // dst_row = row_off + n * row_stride
+  uint8_t* ref_codes;       // optional reference-layout packed codes (flat, even in low nibble)
+  float* ref_scales;        // optional reference-layout scales [rows, G]
+};
+
+struct SeqState {
+  int* pending;
+  int* committed;
+  int* n_out;
+  int* done;
+  int* finish;      // 0 running, 1 eos, 2 max_new_tokens
+  int* max_new;
+  int* g_eff;
+  int* drafted;     // [B][gamma]
+  int* out_tokens;  // [B][out_cap]
+  int* n_drafted;
+  int* n_accepted;
+  int* n_cycles;
+  int* dropped;
+  int* trace;       // [B][trace_cap][4]: drafted_len, accept_len, kept_len, is_bonus
+  int* trace_tok;   // [B][trace_cap][gamma]
+  int out_cap, trace_cap;
+  int B, gamma, eos, max_seq;
+  int* tok;         // forward inputs
+  int* pos;
+  int* slot;
+  const int* argmax;  // forward output
+};
+
+}  // namespace qs

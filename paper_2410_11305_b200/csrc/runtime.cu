@@ -1,0 +1,411 @@
+// C-ABI entry points and the native step runtime (qs_forward): the per-layer
+// launch sequence of model.py:255-348 over device-resident weights and the
+// shared paged KV cache.  No allocation, no synchronisation: everything is
+// enqueued on the caller's stream, so the Python engine can capture whole
+// draft/verify cycles into CUDA graphs.
+#include <cmath>
+#include <cstdio>
+
+#include "../../include/qspec_b200.h"
+#include "qs_common.cuh"
+
+namespace qs {
+cudaError_t launch_linear(int L, const LinearArgs& a, cudaStream_t st);
+cudaError_t launch_act_pack(int L, const PackArgs& a, cudaStream_t st);
+cudaError_t launch_attention(const AttnArgs& a, int n_blk, cudaStream_t st);
+size_t attention_smem_bytes(int qmax, int hpk, int hd, int ctx_cap);
+
+cudaError_t launch_quantize_weight(const QuantWArgs& a, cudaStream_t st);
+cudaError_t launch_lcg_fill(float* out, unsigned long long seed, unsigned long long offset, long long count,
+                            float scale, cudaStream_t st);
+cudaError_t launch_repack_ref(const uint8_t* ref_codes, const float* ref_scales, int rows, int cols, int g,
+                              uint8_t* codes, float* scales, int n_pad, int n_chunks, int gp, int G, int row_off,
+                              int row_stride, cudaStream_t st);
+
+cudaError_t launch_control(int op, const SeqState& s, int j, cudaStream_t st);
+}  // namespace qs
+
+using namespace qs;
+
+namespace {
+
+constexpr int kMaxT = 64;
+
+int g_num_sms = 0;
+
+int num_sms() {
+  if (g_num_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+int status(cudaError_t e) {
+  if (e == cudaSuccess) return QS_OK;
+  fprintf(stderr, "[qspec_b200] CUDA error: %s\n", cudaGetErrorString(e));
+  return QS_ERR_CUDA;
+}
+
+void fill_geometry(int n, int k, int g, qs_qweight_t* w) {
+  w->n = n;
+  w->k = k;
+  w->g = g;
+  w->n_pad = round_up(n, kTileN);
+  w->n_tiles = w->n_pad / kTileN;
+  w->G = k / g;
+  w->gp = round_up(g, kChunkK);
+  w->cpg = w->gp / kChunkK;
+  w->n_chunks = w->G * w->cpg;
+}
+
+PackArgs pack_args(const qs_qweight_t& w, const float* x, int ldx, int T, const qs_workspace_t* ws, int L) {
+  PackArgs p{};
+  p.x = x;
+  p.ldx = ldx;
+  p.T = T;
+  p.K = w.k;
+  p.g = w.g;
+  p.gp = w.gp;
+  p.G = w.G;
+  p.n_chunks = w.n_chunks;
+  p.r_pad = img_rows(T, L);
+  p.a_ld = round_up(T, 8);
+  p.img = ws->img;
+  p.ascale = ws->ascale;
+  return p;
+}
+
+LinearArgs linear_args(const qs_qweight_t& w, int T, int L, const qs_workspace_t* ws, int op, float* out,
+                       int ldo) {
+  LinearArgs a{};
+  a.codes = w.codes;
+  a.wscale = w.scales;
+  a.act = ws->img;
+  a.ascale = ws->ascale;
+  a.n = w.n;
+  a.n_pad = w.n_pad;
+  a.n_tiles = w.n_tiles;
+  a.G = w.G;
+  a.cpg = w.cpg;
+  a.n_chunks = w.n_chunks;
+  a.T = T;
+  a.r_pad = img_rows(T, L);
+  a.a_ld = round_up(T, 8);
+  const int U = w.n_tiles * w.G;
+  a.n_cta = U < num_sms() ? U : num_sms();
+  a.part = ws->part;
+  a.counters = ws->counters;
+  a.op = op;
+  a.out = out;
+  a.ldo = ldo;
+  a.arg_val = ws->arg_val;
+  a.arg_idx = ws->arg_idx;
+  return a;
+}
+
+int check_weight(const qs_qweight_t* w) {
+  if (!w || !w->codes || !w->scales) return QS_ERR_SHAPE;
+  if (w->g < 1 || w->k % w->g != 0) return QS_ERR_CONFIG;
+  return QS_OK;
+}
+
+int run_linear(const qs_qweight_t* w, const float* x, int T, float* y, const qs_workspace_t* ws, int L, int op,
+               int32_t* dump, cudaStream_t st) {
+  int rc = check_weight(w);
+  if (rc) return rc;
+  if (T < 1 || T > kMaxT || !x || !ws) return QS_ERR_SHAPE;
+  PackArgs p = pack_args(*w, x, w->k, T, ws, L);
+  cudaError_t e = launch_act_pack(L, p, st);
+  if (e != cudaSuccess) return status(e);
+  LinearArgs a = linear_args(*w, T, L, ws, op, y, w->n);
+  a.dump = dump;
+  return status(launch_linear(L, a, st));
+}
+
+SeqState seq_state(const qs_seq_t* s) {
+  SeqState q;
+  q.pending = s->pending;
+  q.committed = s->committed;
+  q.n_out = s->n_out;
+  q.done = s->done;
+  q.finish = s->finish;
+  q.max_new = s->max_new;
+  q.g_eff = s->g_eff;
+  q.drafted = s->drafted;
+  q.out_tokens = s->out_tokens;
+  q.n_drafted = s->n_drafted;
+  q.n_accepted = s->n_accepted;
+  q.n_cycles = s->n_cycles;
+  q.dropped = s->dropped;
+  q.trace = s->trace;
+  q.trace_tok = s->trace_tok;
+  q.out_cap = s->out_cap;
+  q.trace_cap = s->trace_cap;
+  q.B = s->B;
+  q.gamma = s->gamma;
+  q.eos = s->eos;
+  q.max_seq = s->max_seq;
+  q.tok = s->tok;
+  q.pos = s->pos;
+  q.slot = s->slot;
+  q.argmax = s->argmax;
+  return q;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* qs_version(void) { return "qspec_b200 0.1 (sm_100a tcgen05 kind::i8)"; }
+
+int qs_num_sms(int32_t* out) {
+  *out = num_sms();
+  return QS_OK;
+}
+
+int qs_linear_max_tokens(void) { return kMaxT; }
+
+int qs_qweight_geometry(int32_t n, int32_t k, int32_t g, qs_qweight_t* out) {
+  if (n < 1 || k < 1 || g < 1 || k % g != 0) return QS_ERR_CONFIG;
+  fill_geometry(n, k, g, out);
+  out->codes = nullptr;
+  out->scales = nullptr;
+  return QS_OK;
+}
+
+int qs_workspace_size(const qs_model_t* m, int32_t t_max, qs_workspace_sizes_t* out) {
+  if (t_max < 1 || t_max > kMaxT) return QS_ERR_SHAPE;
+  const int hd = m->d_model / m->n_heads;
+  qs_qweight_t wd, wf, wl;
+  fill_geometry(m->d_model, m->d_model, m->group_size, &wd);
+  fill_geometry(m->d_model, m->d_ff, m->group_size, &wf);
+  fill_geometry(m->vocab, m->d_model, m->group_size, &wl);
+  const int chunks = wd.n_chunks > wf.n_chunks ? wd.n_chunks : wf.n_chunks;
+  const int groups = wd.G > wf.G ? wd.G : wf.G;
+  int tiles = wl.n_tiles;
+  const int t_ff = round_up(2 * m->d_ff, kTileN) / kTileN;
+  const int t_qkv = round_up((m->n_heads + 2 * m->n_kv_heads) * hd, kTileN) / kTileN;
+  if (t_ff > tiles) tiles = t_ff;
+  if (t_qkv > tiles) tiles = t_qkv;
+  out->x = (size_t)t_max * m->d_model * 4;
+  out->h = (size_t)t_max * m->d_ff * 4;
+  out->attn = (size_t)t_max * m->d_model * 4;
+  out->q = (size_t)t_max * m->n_heads * hd * 4;
+  out->img = (size_t)chunks * img_rows(kMaxT, 3) * 128;
+  out->ascale = (size_t)groups * kMaxT * 4;
+  out->part = (size_t)(num_sms() + tiles) * kMaxT * kTileN * 4;
+  out->counters = (size_t)(tiles + 1) * 4;
+  out->arg_val = (size_t)wl.n_tiles * kMaxT * 4;
+  out->arg_idx = (size_t)wl.n_tiles * kMaxT * 4;
+  return QS_OK;
+}
+
+int qs_init_weight(uint64_t seed, uint64_t draw_offset, float scale, int32_t rows, int32_t cols, int32_t g,
+                   uint8_t* codes, float* scales, int32_t n_pad, int32_t row_off, int32_t row_stride,
+                   uint8_t* ref_codes, float* ref_scales, void* stream) {
+  if (g < 1 || cols % g != 0) return QS_ERR_CONFIG;
+  qs_qweight_t geo;
+  fill_geometry(n_pad, cols, g, &geo);
+  QuantWArgs a{};
+  a.src = nullptr;
+  a.seed = seed;
+  a.offset = draw_offset;
+  a.scale = scale;
+  a.rows = rows;
+  a.cols = cols;
+  a.g = g;
+  a.codes = codes;
+  a.scales = scales;
+  a.n_pad = n_pad;
+  a.n_chunks = geo.n_chunks;
+  a.gp = geo.gp;
+  a.G = geo.G;
+  a.row_off = row_off;
+  a.row_stride = row_stride;
+  a.ref_codes = ref_codes;
+  a.ref_scales = ref_scales;
+  return status(launch_quantize_weight(a, (cudaStream_t)stream));
+}
+
+int qs_quantize_weight(const float* w, int32_t rows, int32_t cols, int32_t g, uint8_t* codes, float* scales,
+                       int32_t n_pad, int32_t row_off, int32_t row_stride, uint8_t* ref_codes, float* ref_scales,
+                       void* stream) {
+  if (g < 1 || cols % g != 0) return QS_ERR_CONFIG;
+  if (!w) return QS_ERR_SHAPE;
+  qs_qweight_t geo;
+  fill_geometry(n_pad, cols, g, &geo);
+  QuantWArgs a{};
+  a.src = w;
+  a.rows = rows;
+  a.cols = cols;
+  a.g = g;
+  a.codes = codes;
+  a.scales = scales;
+  a.n_pad = n_pad;
+  a.n_chunks = geo.n_chunks;
+  a.gp = geo.gp;
+  a.G = geo.G;
+  a.row_off = row_off;
+  a.row_stride = row_stride;
+  a.ref_codes = ref_codes;
+  a.ref_scales = ref_scales;
+  return status(launch_quantize_weight(a, (cudaStream_t)stream));
+}
+
+int qs_lcg_fill(float* out, uint64_t seed, uint64_t draw_offset, int64_t count, float scale, void* stream) {
+  if (count <= 0) return QS_OK;
+  return status(launch_lcg_fill(out, seed, draw_offset, count, scale, (cudaStream_t)stream));
+}
+
+int qs_repack_ref(const uint8_t* ref_codes, const float* ref_scales, int32_t rows, int32_t cols, int32_t g,
+                  uint8_t* codes, float* scales, int32_t n_pad, int32_t row_off, int32_t row_stride, void* stream) {
+  if (g < 1 || cols % g != 0) return QS_ERR_CONFIG;
+  qs_qweight_t geo;
+  fill_geometry(n_pad, cols, g, &geo);
+  return status(launch_repack_ref(ref_codes, ref_scales, rows, cols, g, codes, scales, n_pad, geo.n_chunks, geo.gp,
+                                  geo.G, row_off, row_stride, (cudaStream_t)stream));
+}
+
+int qs_act_quant(const float* x, int32_t T, int32_t K, int32_t g, int8_t* codes, float* scales, float* fq,
+                 void* stream) {
+  if (g < 1 || K % g != 0) return QS_ERR_CONFIG;
+  if (T < 1 || !x) return QS_ERR_SHAPE;
+  PackArgs p{};
+  p.x = x;
+  p.ldx = K;
+  p.T = T;
+  p.K = K;
+  p.g = g;
+  p.gp = round_up(g, kChunkK);
+  p.G = K / g;
+  p.codes_out = codes;
+  p.scales_out = scales;
+  p.fq_out = fq;
+  return status(launch_act_pack(1, p, (cudaStream_t)stream));
+}
+
+int qs_w4a4_linear(const qs_qweight_t* w, const float* x, int32_t T, float* y, const qs_workspace_t* ws,
+                   void* stream) {
+  return run_linear(w, x, T, y, ws, 1, kOpStore, nullptr, (cudaStream_t)stream);
+}
+
+int qs_w4a16_linear(const qs_qweight_t* w, const float* x, int32_t T, float* y, const qs_workspace_t* ws,
+                    void* stream) {
+  return run_linear(w, x, T, y, ws, 3, kOpStore, nullptr, (cudaStream_t)stream);
+}
+
+int qs_linear_group_dots(const qs_qweight_t* w, const float* x, int32_t T, int32_t mode, int32_t* dots,
+                         const qs_workspace_t* ws, void* stream) {
+  return run_linear(w, x, T, nullptr, ws, mode == QS_MODE_LOW ? 1 : 3, kOpDump, dots, (cudaStream_t)stream);
+}
+
+int qs_forward(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const qs_workspace_t* ws, float* logits,
+               int32_t* argmax, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const int T = b->T;
+  if (T < 1 || T > kMaxT) return QS_ERR_SHAPE;
+  const int L = mode == QS_MODE_LOW ? 1 : 3;
+  const int d = m->d_model, H = m->n_heads, KV = m->n_kv_heads, hd = d / H, ff = m->d_ff;
+  const int hpk = H / KV;
+  if (b->blk_qmax * hpk > 64 || b->blk_qmax * hpk * hd > 8192) return QS_ERR_SHAPE;
+  if (attention_smem_bytes(b->blk_qmax, hpk, hd, b->ctx_cap) > 200 * 1024) return QS_ERR_SHAPE;
+  cudaError_t e;
+  for (int li = 0; li < m->n_layers; ++li) {
+    const qs_layer_t& ly = m->layers[li];
+    // attn rmsnorm (+ embedding gather on layer 0) -> activation operand
+    PackArgs p = pack_args(ly.qkv, ws->x, d, T, ws, L);
+    p.rms_w = ly.attn_norm;
+    p.eps = m->norm_eps;
+    if (li == 0) {
+      p.gather_ids = b->tokens;
+      p.emb = m->tok_emb;
+      p.x_out = ws->x;
+    }
+    if ((e = launch_act_pack(L, p, st)) != cudaSuccess) return status(e);
+    // q|k|v projection, fused RoPE + KV write (model.py:305-309, 339-340)
+    LinearArgs a = linear_args(ly.qkv, T, L, ws, kOpQkvRope, ws->q, H * hd);
+    a.pos = b->positions;
+    a.slot = b->slots;
+    a.rope_cos = m->rope_cos;
+    a.rope_sin = m->rope_sin;
+    a.hd = hd;
+    a.n_q = H * hd;
+    a.n_k = KV * hd;
+    a.n_kv_heads = KV;
+    a.kcache = ly.k_cache;
+    a.vcache = ly.v_cache;
+    a.block_table = m->block_table;
+    a.bt_ld = m->bt_ld;
+    a.page = m->page;
+    if ((e = launch_linear(L, a, st)) != cudaSuccess) return status(e);
+    // attention (model.py:293-330)
+    AttnArgs at{};
+    at.q = ws->q;
+    at.ldq = H * hd;
+    at.kcache = ly.k_cache;
+    at.vcache = ly.v_cache;
+    at.block_table = m->block_table;
+    at.bt_ld = m->bt_ld;
+    at.page = m->page;
+    at.pos = b->positions;
+    at.slot = b->slots;
+    at.blk_tok0 = b->blk_tok0;
+    at.blk_ntok = b->blk_ntok;
+    at.H = H;
+    at.KV = KV;
+    at.hd = hd;
+    at.hpk = hpk;
+    at.inv_sqrt_hd = 1.0f / sqrtf((float)hd);
+    at.qmax = b->blk_qmax;
+    at.ctx_cap = b->ctx_cap;
+    at.out = ws->attn;
+    at.ldo = d;
+    if ((e = launch_attention(at, b->n_blk, st)) != cudaSuccess) return status(e);
+    // o_proj + residual (model.py:332)
+    p = pack_args(ly.o, ws->attn, d, T, ws, L);
+    if ((e = launch_act_pack(L, p, st)) != cudaSuccess) return status(e);
+    a = linear_args(ly.o, T, L, ws, kOpResidual, ws->x, d);
+    if ((e = launch_linear(L, a, st)) != cudaSuccess) return status(e);
+    // ffn rmsnorm -> gate|up with fused silu * up (model.py:333-335)
+    p = pack_args(ly.gate_up, ws->x, d, T, ws, L);
+    p.rms_w = ly.ffn_norm;
+    p.eps = m->norm_eps;
+    if ((e = launch_act_pack(L, p, st)) != cudaSuccess) return status(e);
+    a = linear_args(ly.gate_up, T, L, ws, kOpSiluMul, ws->h, ff);
+    if ((e = launch_linear(L, a, st)) != cudaSuccess) return status(e);
+    // down_proj + residual (model.py:336)
+    p = pack_args(ly.down, ws->h, ff, T, ws, L);
+    if ((e = launch_act_pack(L, p, st)) != cudaSuccess) return status(e);
+    a = linear_args(ly.down, T, L, ws, kOpResidual, ws->x, d);
+    if ((e = launch_linear(L, a, st)) != cudaSuccess) return status(e);
+  }
+  // final norm + lm_head + argmax (model.py:342-344, numerics.py:81-86)
+  PackArgs p = pack_args(m->lm_head, ws->x, d, T, ws, L);
+  p.rms_w = m->final_norm;
+  p.eps = m->norm_eps;
+  if ((e = launch_act_pack(L, p, st)) != cudaSuccess) return status(e);
+  LinearArgs a = linear_args(m->lm_head, T, L, ws, kOpLogits, logits, m->vocab);
+  a.argmax_out = argmax;
+  return status(launch_linear(L, a, st));
+}
+
+int qs_draft_prep(const qs_seq_t* s, int32_t step, void* stream) {
+  return status(launch_control(0, seq_state(s), step, (cudaStream_t)stream));
+}
+int qs_verify_prep(const qs_seq_t* s, void* stream) {
+  return status(launch_control(1, seq_state(s), 0, (cudaStream_t)stream));
+}
+int qs_accept(const qs_seq_t* s, void* stream) {
+  return status(launch_control(2, seq_state(s), 0, (cudaStream_t)stream));
+}
+int qs_ar_prep(const qs_seq_t* s, void* stream) {
+  return status(launch_control(3, seq_state(s), 0, (cudaStream_t)stream));
+}
+int qs_ar_commit(const qs_seq_t* s, void* stream) {
+  return status(launch_control(4, seq_state(s), 0, (cudaStream_t)stream));
+}
+
+}  // extern "C"

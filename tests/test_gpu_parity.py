@@ -1,0 +1,231 @@
+"""GPU parity: the sm_100a path against the CPU oracle (which is pinned to the reference).
+
+Bars:
+  * integer / byte work bit-exact: LCG weights, packed codes, scales, activation
+    codes and scales, tensor-core group dots;
+  * fp32 outputs of the linear within 2e-5 of max|y| (north star: 1e-2 relative);
+  * logits within 1e-2 relative, greedy tokens identical to the oracle.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import MODEL_SPECS, TINY, conftest_cfg
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover - CPU container
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2410_11305_b200 as Q  # noqa: E402
+from oracle import qspec_oracle as O  # noqa: E402
+
+HIGH, LOW = Q.ExecutionMode.HIGH_PRECISION, Q.ExecutionMode.LOW_PRECISION
+
+_cache: dict = {}
+
+
+def models(cfg_kw: dict, seed: int):
+    key = (tuple(sorted(cfg_kw.items())), seed)
+    if key not in _cache:
+        _cache[key] = (Q.random_init(Q.ModelConfig(**cfg_kw), seed), O.random_model(O.OracleConfig(**cfg_kw), seed))
+    return _cache[key]
+
+
+# ----------------------------------------------------------------- byte / integer exactness
+def test_library_loaded_and_sm100():
+    from paper_2410_11305_b200 import _lib
+    assert b"sm_100a" in _lib.load().qs_version()
+    assert torch.cuda.get_device_capability() == (10, 0)
+
+
+@pytest.mark.parametrize("gs", [16, 32, 128])
+def test_act_quant_bit_exact(golden, gs):
+    x = torch.from_numpy(golden[f"aq{gs}.x"]).cuda()
+    fq, codes, scales = Q.fake_quantize_activations(x, gs, return_codes=True)
+    assert np.array_equal(codes.cpu().numpy(), golden[f"aq{gs}.codes"])
+    assert np.array_equal(scales.cpu().numpy(), golden[f"aq{gs}.scales"])
+    assert np.array_equal(fq.cpu().numpy(), golden[f"aq{gs}.fq"])
+
+
+def test_act_quant_random_large():
+    rng = np.random.default_rng(3)
+    x = (rng.standard_normal((7, 11008)) * rng.uniform(0.01, 5, size=(7, 1))).astype(np.float32)
+    x[2, 128:256] = 0.0
+    c_ref, s_ref = O.quantize_rows(x, 128)
+    _, c, s = Q.fake_quantize_activations(torch.from_numpy(x).cuda(), 128, return_codes=True)
+    assert np.array_equal(c.cpu().numpy(), c_ref) and np.array_equal(s.cpu().numpy(), s_ref)
+
+
+def test_random_init_matches_golden(golden):
+    m = Q.random_init(Q.ModelConfig(**conftest_cfg()), 0)
+    assert np.array_equal(m.token_embedding.cpu().numpy(), golden["toy0.token_embedding"])
+    for name, q in m.quantized_tensors():
+        assert np.array_equal(q.codes, golden[f"toy0.{name}.codes"]), name
+        assert np.array_equal(q.scales, golden[f"toy0.{name}.scales"]), name
+
+
+def test_random_init_golden_q_proj():
+    # pkg/tests/test_storage_cli.py:31-39
+    m = Q.random_init(Q.ModelConfig(**conftest_cfg(max_seq_len=128)), 42)
+    assert m.layers[0].q_proj.codes[:16].tobytes() == bytes(
+        [147, 189, 11, 13, 82, 207, 165, 234, 188, 52, 201, 74, 195, 167, 86, 207])
+
+
+def test_random_init_tiny_digests(golden):
+    import hashlib
+    m = Q.random_init(Q.ModelConfig(**TINY), 0)
+    sha = lambda a: hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()  # noqa: E731
+    got = [f"{n}:{sha(q.codes)}:{sha(q.scales)}" for n, q in m.quantized_tensors()]
+    assert got == [str(s) for s in golden["tiny.digests"]]
+    assert sha(m.token_embedding.cpu().numpy()) == str(golden["tiny.emb_digest"][0])
+
+
+@pytest.mark.parametrize("n,k,g,T", [(256, 512, 128, 1), (384, 4096, 128, 5), (320, 256, 32, 16),
+                                     (128, 192, 48, 3), (4096, 4096, 128, 64), (11008, 4096, 128, 4)])
+def test_integer_core_exact_low(n, k, g, T):
+    rng = np.random.default_rng(n + k + T)
+    w = (rng.standard_normal((n, k)) * 0.02).astype(np.float32)
+    x = rng.standard_normal((T, k)).astype(np.float32)
+    q = Q.quantize_groupwise(torch.from_numpy(w), g)
+    wc, _ = O.quantize_rows(w, g)
+    xc, _ = O.quantize_rows(x, g)
+    dots = Q.quant.linear_group_dots(q, torch.from_numpy(x), LOW).cpu().numpy()
+    G = k // g
+    ref = np.einsum("ngk,tgk->ngt", wc.reshape(n, G, g).astype(np.int64), xc.reshape(T, G, g).astype(np.int64))
+    assert np.array_equal(dots[:n, :, :T], ref)
+
+
+@pytest.mark.parametrize("n,k,g,T", [(256, 512, 128, 2), (11008, 4096, 128, 16), (320, 256, 32, 21)])
+def test_integer_core_exact_high_limbs(n, k, g, T):
+    rng = np.random.default_rng(7 * n + T)
+    w = (rng.standard_normal((n, k)) * 0.02).astype(np.float32)
+    x = rng.standard_normal((T, k)).astype(np.float32)
+    q = Q.quantize_groupwise(torch.from_numpy(w), g)
+    wc, _ = O.quantize_rows(w, g)
+    G = k // g
+    xg = x.reshape(T, G, g)
+    m = np.abs(xg).max(-1)
+    e = 22 - np.frexp(m)[1]
+    X = np.rint(np.ldexp(xg.astype(np.float64), e[:, :, None])).astype(np.int64)
+    l0 = ((X + 128) & 255) - 128
+    X1 = (X - l0) >> 8
+    l1 = ((X1 + 128) & 255) - 128
+    l2 = (X1 - l1) >> 8
+    dots = Q.quant.linear_group_dots(q, torch.from_numpy(x), HIGH).cpu().numpy()
+    wg = wc.reshape(n, G, g).astype(np.int64)
+    for li, limb in enumerate((l0, l1, l2)):
+        ref = np.einsum("ngk,tgk->ngt", wg, limb)
+        assert np.array_equal(dots[:n, :, li:3 * T:3], ref), f"limb {li}"
+
+
+# ----------------------------------------------------------------- fp32 linear vs oracle
+@pytest.mark.parametrize("mode", [LOW, HIGH])
+@pytest.mark.parametrize("n,k,g,T", [(384, 4096, 128, 1), (11008, 4096, 128, 16), (4096, 11008, 128, 64),
+                                     (96, 64, 32, 3), (1024, 256, 128, 80)])
+def test_qlinear_vs_oracle(mode, n, k, g, T):
+    rng = np.random.default_rng(n * 3 + T)
+    w = (rng.standard_normal((n, k)) / np.sqrt(k)).astype(np.float32)
+    x = rng.standard_normal((T, k)).astype(np.float32)
+    q = Q.quantize_groupwise(torch.from_numpy(w), g)
+    wc, ws = O.quantize_rows(w, g)
+    lin = O.OracleLinear(wc, ws, g)
+    ref = O.qlinear(lin, x, mode is LOW)
+    y = Q.qlinear_forward(q, torch.from_numpy(x), mode).cpu().numpy()
+    tol = 2e-5 * np.abs(ref).max()
+    assert np.abs(y - ref).max() <= tol, np.abs(y - ref).max() / np.abs(ref).max()
+
+
+def test_qlinear_batch_invariance():
+    rng = np.random.default_rng(11)
+    w = (rng.standard_normal((512, 1024)) * 0.03).astype(np.float32)
+    x = rng.standard_normal((40, 1024)).astype(np.float32)
+    q = Q.quantize_groupwise(torch.from_numpy(w), 128)
+    for mode in (LOW, HIGH):
+        full = Q.qlinear_forward(q, torch.from_numpy(x), mode).cpu().numpy()
+        for i in (0, 7, 39):
+            one = Q.qlinear_forward(q, torch.from_numpy(x[i:i + 1]), mode).cpu().numpy()
+            assert np.array_equal(full[i:i + 1], one)
+
+
+# ----------------------------------------------------------------- forward / generation
+@pytest.mark.parametrize("mode", [HIGH, LOW])
+def test_forward_logits_vs_golden(golden, mode):
+    m = Q.random_init(Q.ModelConfig(**conftest_cfg()), 0)
+    kv = Q.KVCache(m.config)
+    blk = Q.forward(m, [5, 9, 200, 3, 77], kv, mode, Q.WriteTarget.VERIFY)
+    ref = golden["fwd.high" if mode is HIGH else "fwd.low"]
+    got = blk.numpy()
+    assert np.abs(got - ref).max() <= 1e-2 * np.abs(ref).max()
+    if mode is HIGH:
+        assert np.abs(got - ref).max() <= 1e-4 * np.abs(ref).max()
+        assert list(np.argmax(got, -1)) == list(np.argmax(ref, -1))
+        k0 = kv.rows(0, 0, 5, "k").cpu().numpy()
+        assert np.abs(k0 - golden["fwd.high.k0"]).max() <= 1e-4 * np.abs(golden["fwd.high.k0"]).max()
+
+
+def test_forward_batched_equals_chained():
+    # pkg/tests/test_model.py:89-105 on the device: bit-identical logits and KV
+    m = Q.random_init(Q.ModelConfig(**conftest_cfg(n_kv_heads=2)), 0)
+    toks = [5, 9, 200, 3, 77]
+    kv_a, kv_b = Q.KVCache(m.config), Q.KVCache(m.config)
+    block = Q.forward(m, toks, kv_a, HIGH, Q.WriteTarget.VERIFY).numpy()
+    rows = [Q.forward(m, [t], kv_b, HIGH, Q.WriteTarget.VERIFY).numpy()[0] for t in toks]
+    assert np.array_equal(block, np.stack(rows))
+    for li in range(m.config.n_layers):
+        assert torch.equal(kv_a.rows(li, 0, 5, "k"), kv_b.rows(li, 0, 5, "k"))
+        assert torch.equal(kv_a.rows(li, 0, 5, "v"), kv_b.rows(li, 0, 5, "v"))
+
+
+def test_tiny_greedy_and_qspec_tokens(golden):
+    m = Q.random_init(Q.ModelConfig(**TINY), 0)
+    prompts = golden["tiny.prompts"]
+    for i in range(len(prompts)):
+        p = [int(t) for t in prompts[i]]
+        ref = [int(t) for t in golden["tiny.greedy"][i]]
+        gr = Q.generate_greedy(m, p, HIGH, Q.GenerationConfig(max_new_tokens=64))
+        assert gr.new_tokens == ref, f"greedy prompt {i}"
+        qs = Q.generate_qspec(m, p, Q.GenerationConfig(gamma=3, max_new_tokens=64))
+        assert qs.new_tokens == ref, f"qspec prompt {i}"
+
+
+def test_toy_gamma_sweep(golden):
+    m = Q.random_init(Q.ModelConfig(**conftest_cfg(vocab_size=512)), 6)
+    ref = [int(t) for t in golden["toy6.greedy"]]
+    for gm in (1, 2, 3, 5, 7):
+        r = Q.generate_qspec(m, [4, 9, 100, 3], Q.GenerationConfig(gamma=gm, max_new_tokens=14))
+        assert r.new_tokens == ref, gm
+
+
+def test_self_draft_accepts_everything():
+    # pkg/tests/test_acceptance.py:155-169 (C4): needs GPU batch invariance
+    m = Q.random_init(Q.ModelConfig(**conftest_cfg(max_seq_len=64)), 4)
+    for gm in range(1, 8):
+        cfg = Q.GenerationConfig(gamma=gm, max_new_tokens=3 * (gm + 1) + 1, draft_mode=HIGH)
+        r = Q.generate_qspec(m, [1, 2, 3], cfg)
+        assert r.acceptance_rate == 1.0 and r.tokens_per_cycle == gm + 1, gm
+
+
+@pytest.mark.parametrize("mi", range(len(MODEL_SPECS)))
+def test_acceptance_shapes_tokens(golden, mi):
+    cfg = Q.ModelConfig(**conftest_cfg(max_seq_len=48, **MODEL_SPECS[mi]))
+    m = Q.random_init(cfg, 1000 + mi)
+    for pi in range(3):
+        p = [int(t) for t in golden[f"spec{mi}.p{pi}.prompt"]]
+        ref = [int(t) for t in golden[f"spec{mi}.p{pi}.greedy"]]
+        for gm in (1, 3, 7):
+            assert Q.generate_qspec(m, p, Q.GenerationConfig(gamma=gm, max_new_tokens=12)).new_tokens == ref
+
+
+def test_phase_api_matches_engine():
+    m = Q.random_init(Q.ModelConfig(**conftest_cfg(vocab_size=512)), 6)
+    eng = Q.SequenceEngine(m, [4, 9, 100, 3], Q.GenerationConfig(gamma=3, max_new_tokens=14))
+    eng.prefill()
+    while not eng.done:
+        eng.run_cycle()
+    fast = Q.generate_qspec(m, [4, 9, 100, 3], Q.GenerationConfig(gamma=3, max_new_tokens=14))
+    assert eng.tokens == fast.tokens
+    assert eng.result().acceptance_rate == fast.acceptance_rate
