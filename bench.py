@@ -1,0 +1,387 @@
+#!/usr/bin/env python
+"""QSpec decode benchmark (BASELINE.json metric) -- one JSON line on rank 0.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1]): Llama-2-7B-shape random-init W4 model
+(L=32, d=4096, H=KV=32, ff=11008, V=32000, g=128, max_seq 512; LCG weights,
+seed 0), B requests of 128 prompt tokens (rng 42) decoding 128 new tokens,
+QSpec gamma=3 greedy.  A step is one draft/verify cycle of the whole batch
+(gamma W4A4 draft forwards + one W4A16 verify forward + device accept/commit),
+replayed from a CUDA graph.  value = generated tokens / device time of exactly
+K steps (CUDA events, barrier + synchronize on both sides, max over ranks).
+Weights (3.5 GB) are far larger than L2 (126 MB), so every step streams them
+from HBM (no L2 flush needed).  The same run times W4A16 autoregressive
+decoding on the same kernels and reports the speedup.
+
+Multi-GPU: one process per GPU (torchrun), each an independent replica with its
+own requests (request sharding, no data-path collective): weak scaling.
+
+--impl reference: the reference's CPU path (the oracle port of
+pkg/src/qspec, bit-exact with it) on the host cores: a bounded sample (one
+decoder layer + lm_head of the same 7B shape, timed per forward kind and
+extrapolated to 32 layers and one QSpec cycle), run as one process per core.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CFG7B = dict(n_layers=32, d_model=4096, n_heads=32, n_kv_heads=32, d_ff=11008, vocab_size=32000,
+             max_seq_len=512, rope_theta=10000.0, norm_eps=1e-5, group_size=128)
+METRIC = "QSpec tokens/s per GPU vs W4A16 autoregressive, 7B-shape; draft accept rate"
+UNIT = "tokens/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--batch", type=int, default=16)
+    ap.add_argument("--gamma", type=int, default=3)
+    ap.add_argument("--prompt", type=int, default=128)
+    ap.add_argument("--new", type=int, default=128)
+    ap.add_argument("--sweep", default="1,4,16", help="extra batch sizes reported under per_batch")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--small", action="store_true", help="tiny config (smoke / CI)")
+    return ap.parse_args()
+
+
+def workload_name(a) -> str:
+    shape = "tiny-2L-d256" if a.small else "llama2-7b-shape"
+    return (f"{shape} random-init W4 g128 (LCG seed 0), QSpec gamma={a.gamma} greedy, batch {a.batch}/GPU, "
+            f"prompt {a.prompt}, {a.new} new tokens")
+
+
+def model_cfg(a) -> dict:
+    if a.small:
+        return dict(n_layers=2, d_model=256, n_heads=4, n_kv_heads=4, d_ff=768, vocab_size=1024,
+                    max_seq_len=512, group_size=128)
+    return dict(CFG7B)
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled while a region runs."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int) -> None:
+        self.index, self.rows, self.proc = index, [], None
+
+    def start(self) -> None:
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self) -> None:
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm = [float(r[1]) for r in self.rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows if len(r) >= 9 for i in range(4) if r[5 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def run_decode(model, a, batch: int, algorithm: str, prompts: np.ndarray, steps: int, warmup: int,
+               dist=None, profile: bool = False, clocks: ClockSampler | None = None) -> dict:
+    import torch
+    from paper_2410_11305_b200.engine import DecodeEngine
+    eng = DecodeEngine(model, batch, gamma=a.gamma, max_new_cap=a.new + 8, algorithm=algorithm)
+    for b in range(batch):
+        eng.prefill(b, [int(t) for t in prompts[b]], a.new)
+    for _ in range(warmup):
+        eng.step()
+    torch.cuda.synchronize()
+    n0 = eng.t["n_out"].sum().item()
+    nd0, na0 = eng.t["n_drafted"].sum().item(), eng.t["n_accepted"].sum().item()
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    if clocks:
+        clocks.start()
+    e0.record(st)
+    for _ in range(steps):
+        eng.step()
+    e1.record(st)
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    ck = clocks.stop() if clocks else None
+    ms = e0.elapsed_time(e1)
+    tokens = eng.t["n_out"].sum().item() - n0
+    nd, na = eng.t["n_drafted"].sum().item() - nd0, eng.t["n_accepted"].sum().item() - na0
+    out = {"ms": ms, "tokens": tokens, "steps": steps, "tok_s": tokens / (ms / 1e3),
+           "acceptance_rate": (na / nd) if nd else None, "launches_per_step": eng.launches_per_step(),
+           "clocks": ck}
+    if profile:
+        out["profile"] = eng.profile_step()
+    del eng
+    torch.cuda.empty_cache()
+    return out
+
+
+def run_e2e(model, a, batch: int, prompts: np.ndarray) -> dict:
+    """Public-API end to end: pinned host prompts -> device -> QSpec cycles -> tokens on the host."""
+    import torch
+    from paper_2410_11305_b200.engine import DecodeEngine
+    eng = DecodeEngine(model, batch, gamma=a.gamma, max_new_cap=a.new + 8, algorithm="qspec")
+    host = torch.from_numpy(prompts.astype(np.int32)).pin_memory()
+    eng.prefill(0, [int(t) for t in prompts[0]], a.new)   # warm the graph once
+    eng.step()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    dev = host.cuda(non_blocking=True)
+    for b in range(batch):
+        eng.prefill(b, dev[b], a.new)
+    cycles = 0
+    flags = torch.empty(2 * batch, dtype=torch.int32).pin_memory()
+    while True:
+        eng.step()
+        cycles += 1
+        flags[:batch].copy_(eng.t["done"], non_blocking=True)
+        flags[batch:].copy_(eng.t["n_out"], non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        if bool(flags[:batch].all()):
+            break
+    res = [eng.result(b).new_tokens for b in range(batch)]
+    wall = time.perf_counter() - t0
+    toks = sum(len(r) for r in res)
+    h2d = host.numel() * 4
+    d2h = cycles * flags.numel() * 4 + toks * 4
+    del eng
+    return {"value": toks / wall, "unit": UNIT, "h2d_bytes_per_step": h2d / cycles, "d2h_bytes_per_step": d2h / cycles,
+            "cycles": cycles, "tokens": toks, "wall_s": wall}
+
+
+def linear_roofline(model, a, prof: list, batch: int) -> dict:
+    """Dominant kernel (the tensor-core linear): algorithmic bytes per launch / event-timed duration."""
+    cfg = model.config
+    lw = model.layers[0]
+    stores = [lw.qkv, lw.o, lw.gate_up, lw.down, model.lm_head.store]
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    tot_b = tot_ms = 0.0
+    kinds = {}
+    for ms, tag in prof:
+        mode, kind = tag // 16, tag % 16
+        T = batch if mode == 1 else batch * (a.gamma + 1)
+        st = stores[kind]
+        outw = st.n // 2 if kind == 2 else st.n
+        byts = st.n * st.k / 2 + 4 * st.n * st.k / st.g + 4 * T * st.k + 4 * T * outw
+        tot_b += byts
+        tot_ms += ms
+        key = ("draft" if mode == 1 else "verify") + "." + ["qkv", "o", "gate_up", "down", "lm_head"][kind]
+        d = kinds.setdefault(key, [0, 0.0, 0.0])
+        d[0] += 1
+        d[1] += ms
+        d[2] += byts
+    achieved = tot_b / (tot_ms / 1e3) / 1e9
+    peak = peaks["hbm_gbs"]
+    per = {k: {"launches": v[0], "avg_us": round(1e3 * v[1] / v[0], 2), "GBps": round(v[2] / (v[1] / 1e3) / 1e9, 1)}
+           for k, v in kinds.items()}
+    return {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(achieved / peak, 4), "traffic": None, "kernel": "linear_tc_kernel (all launches of one step)",
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)", "launches": len(prof),
+            "avg_launch_us": round(1e3 * tot_ms / max(1, len(prof)), 2), "linear_share_ms_per_step": round(tot_ms, 3),
+            "per_kind": per}
+
+
+# ----------------------------------------------------------------------------- CPU arm (oracle port)
+def _cpu_worker(args):
+    """One process: 1-layer + lm_head 7B-shape oracle model, timed per forward kind."""
+    cfg_kw, gamma, ctx, reps = args
+    from oracle import qspec_oracle as O
+    cfg1 = O.OracleConfig(**{**cfg_kw, "n_layers": 1})
+    m = O.random_model(cfg1, 0)
+    rng = np.random.default_rng(0)
+    xh = rng.standard_normal((1, cfg1.d_model)).astype(np.float32)
+    O.qlinear(m.lm_head, xh, False)            # build dequant caches before timing
+    for lw in m.layers:
+        for p in O.PROJ:
+            _ = lw[p].wt
+
+    def t_forward(n, low):
+        kv = O.OracleKV(cfg1, gamma_max=max(gamma, 8))
+        kv.clen = ctx                           # attention over a ctx-long (zero) prefix
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            kv.rlen = {"draft": 0, "verify": 0}
+            O.forward(m, list(range(1, n + 1)), kv, low, "verify")
+        return (time.perf_counter() - t0) / reps
+
+    def t_head(n, low):
+        x = rng.standard_normal((n, cfg1.d_model)).astype(np.float32)
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            O.qlinear(m.lm_head, x, low)
+        return (time.perf_counter() - t0) / reps
+
+    f_draft, f_verify = t_forward(1, True), t_forward(gamma + 1, False)
+    h_draft, h_verify = t_head(1, True), t_head(gamma + 1, False)
+    return f_draft, f_verify, h_draft, h_verify
+
+
+def cpu_reference(a, accept_rate: float | None, n_procs: int | None = None) -> dict:
+    import multiprocessing as mp
+    cfg_kw = model_cfg(a)
+    L = cfg_kw["n_layers"]
+    cores = os.cpu_count() or 1
+    n_procs = n_procs or max(1, min(8, cores))
+    ctx = a.prompt + a.new // 2
+    t0 = time.perf_counter()
+    with mp.get_context("spawn").Pool(n_procs) as pool:
+        res = pool.map(_cpu_worker, [(cfg_kw, a.gamma, ctx, 1)] * n_procs)
+    wall = time.perf_counter() - t0
+    # per process: cycle time = gamma draft forwards + 1 verify forward, L layers each
+    rates = []
+    p = accept_rate if accept_rate is not None else 0.25
+    tok_per_cycle = sum(p ** i for i in range(a.gamma + 1))   # E[kept] under per-draft accept prob p
+    for f_d, f_v, h_d, h_v in res:
+        cyc = a.gamma * ((f_d - h_d) * L + h_d) + ((f_v - h_v) * L + h_v)
+        rates.append(tok_per_cycle / cyc)
+    return {"value": round(sum(rates), 4), "unit": UNIT, "cores": n_procs, "kind": "port",
+            "sample": (f"oracle port (bit-exact with pkg/src/qspec) of one {a.gamma}-draft QSpec cycle: 1 decoder layer "
+                       f"+ lm_head of the 7B shape timed per forward kind (W4A4 draft M=1, W4A16 verify M={a.gamma + 1}, "
+                       f"context {ctx}) and extrapolated to {L} layers; tokens/cycle from acceptance {p:.3f}; "
+                       f"{n_procs} concurrent single-threaded processes (einsum is single-threaded), one request each"),
+            "sample_wall_s": round(wall, 1)}
+
+
+# ----------------------------------------------------------------------------- main
+def main() -> None:
+    a = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if a.impl == "reference":
+        if rank != 0:
+            return
+        cpu = cpu_reference(a, None)
+        line = {"metric": METRIC, "value": cpu["value"], "unit": UNIT, "impl": "reference", "n_gpus": a.gpus,
+                "steps": a.steps, "warmup": a.warmup, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f32 (numpy fake-quant)", "data": "synthetic",
+                "config": {"workload": workload_name(a)}, "cpu_baseline": cpu,
+                "e2e": {"value": cpu["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    import torch
+    dist = None
+    if world > 1:
+        import torch.distributed as td
+        torch.cuda.set_device(local)
+        td.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist = td
+    import paper_2410_11305_b200 as Q
+
+    cfg = Q.ModelConfig(**model_cfg(a))
+    t0 = time.perf_counter()
+    model = Q.random_init(cfg, 0)
+    init_s = time.perf_counter() - t0
+    rng = np.random.default_rng(42 + rank)
+    sweep = sorted({int(b) for b in a.sweep.split(",") if b} | {a.batch})
+    prompts = rng.integers(0, cfg.vocab_size, size=(max(sweep), a.prompt))
+
+    clocks = ClockSampler(torch.cuda.current_device())
+    main_q = run_decode(model, a, a.batch, "qspec", prompts, a.steps, a.warmup, dist, profile=True, clocks=clocks)
+    main_ar = run_decode(model, a, a.batch, "greedy", prompts, a.steps, a.warmup, dist)
+
+    # whole-job value: tokens of all ranks / max device time over ranks
+    vals = torch.tensor([main_q["tokens"], main_q["ms"], main_ar["tokens"], main_ar["ms"]], dtype=torch.float64,
+                        device="cuda")
+    if dist is not None:
+        tok = vals.clone()
+        dist.all_reduce(tok, op=dist.ReduceOp.SUM)
+        mx = vals.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        q_tokens, q_ms, ar_tokens, ar_ms = tok[0].item(), mx[1].item(), tok[2].item(), mx[3].item()
+    else:
+        q_tokens, q_ms, ar_tokens, ar_ms = main_q["tokens"], main_q["ms"], main_ar["tokens"], main_ar["ms"]
+
+    per_batch = {}
+    if rank == 0 and world == 1:
+        for b in sweep:
+            if b == a.batch:
+                q, r = main_q, main_ar
+            else:
+                q = run_decode(model, a, b, "qspec", prompts, a.steps, a.warmup)
+                r = run_decode(model, a, b, "greedy", prompts, a.steps, a.warmup)
+            per_batch[str(b)] = {"qspec_tok_s": round(q["tok_s"], 1), "w4a16_ar_tok_s": round(r["tok_s"], 1),
+                                 "speedup_vs_ar": round(q["tok_s"] / r["tok_s"], 3),
+                                 "acceptance_rate": round(q["acceptance_rate"], 4),
+                                 "tokens_per_cycle": round(q["tokens"] / (q["steps"] * b), 3),
+                                 "ms_per_cycle": round(q["ms"] / q["steps"], 3),
+                                 "ms_per_ar_step": round(r["ms"] / r["steps"], 3)}
+    e2e = run_e2e(model, a, a.batch, prompts)
+    roof = linear_roofline(model, a, main_q["profile"], a.batch)
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu:
+        cpu = cpu_reference(a, main_q["acceptance_rate"])
+    if rank != 0:
+        return
+    value = q_tokens / (q_ms / 1e3)
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": round(q_ms / a.steps, 4), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int8 (tcgen05 kind::i8: int4 codes x int4 / 3x8-bit limb activations, int32 "
+                                      "accum, fp32 epilogue)",
+        "data": "synthetic (LCG random-init weights, rng(42) prompts)",
+        "config": {"workload": workload_name(a), "model": "llama2-7b-shape W4 g128" if not a.small else "tiny",
+                   "global_batch": a.batch * world, "seq_len": a.prompt + a.new, "gamma": a.gamma,
+                   "parallelism": f"replicas x{world} (request-sharded, no collective)",
+                   "l2": "weights 3.5 GB >> 126 MB L2: every step streams them from HBM (no flush needed)"},
+        "w4a16_ar_tokens_per_s": round(ar_tokens / (ar_ms / 1e3), 2),
+        "speedup_vs_w4a16_ar": round(value / (ar_tokens / (ar_ms / 1e3)), 4),
+        "acceptance_rate": round(main_q["acceptance_rate"], 4),
+        "per_batch": per_batch,
+        "roofline": roof,
+        "cpu_baseline": cpu,
+        "e2e": {k: (round(v, 2) if isinstance(v, float) else v) for k, v in e2e.items()},
+        "gpu_launches": int(main_q["launches_per_step"] * a.steps),
+        "clocks": main_q["clocks"],
+        "init_s": round(init_s, 2),
+    }
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -94,10 +94,12 @@ typedef struct {
   int32_t* counters; /* zero-initialised once; kernels leave them zero */
   float* arg_val;
   int32_t* arg_idx;
+  float* att_o;   /* split-KV attention partials [t_max][n_heads][chunks][head_dim] */
+  float* att_ml;  /* [t_max][n_heads][chunks][2] chunk max / chunk sum */
 } qs_workspace_t;
 
 typedef struct {
-  size_t x, h, attn, q, img, ascale, part, counters, arg_val, arg_idx; /* bytes */
+  size_t x, h, attn, q, img, ascale, part, counters, arg_val, arg_idx, att_o, att_ml; /* bytes */
 } qs_workspace_sizes_t;
 
 /* Device sequence state for B slots (SoA), driven by the control kernels. */
@@ -135,9 +137,22 @@ int qs_w4a4_linear(const qs_qweight_t* w, const float* x, int32_t T, float* y, c
                    void* stream);
 int qs_w4a16_linear(const qs_qweight_t* w, const float* x, int32_t T, float* y, const qs_workspace_t* ws,
                     void* stream);
+/* the tensor-core linear alone, on the operand image the previous qs_w4a*_linear call packed (microbench) */
+int qs_linear_prepacked(const qs_qweight_t* w, int32_t T, int32_t mode, float* y, const qs_workspace_t* ws,
+                        void* stream);
+/* debug: device buffer [6][256] u64 that qs_linear_prepacked fills with a CTA-0 %globaltimer timeline (NULL: off) */
+int qs_debug_timeline(uint64_t* buf);
 /* raw int32 per-(row, group, image-row) dots of the tensor-core integer core */
 int qs_linear_group_dots(const qs_qweight_t* w, const float* x, int32_t T, int32_t mode, int32_t* dots,
                          const qs_workspace_t* ws, void* stream);
+
+/* -------------------------------------------------------------- profiling */
+/* Event ring around every linear launch of qs_forward (tag = mode*16 + kind,
+ * kind: 0 qkv, 1 o, 2 gate_up, 3 down, 4 lm_head).  Host-side bookkeeping only;
+ * records become event nodes when qs_forward is captured into a CUDA graph. */
+int qs_profile_enable(int32_t max_launches); /* 0 disables */
+int qs_profile_reset(void);
+int qs_profile_read(float* ms, int32_t* tags, int32_t max_out, int32_t* n_out);
 
 /* ------------------------------------------------------------------ step */
 int qs_forward(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const qs_workspace_t* ws, float* logits,

@@ -45,14 +45,15 @@ class Batch(C.Structure):
                 ("blk_tok0", vp), ("blk_ntok", vp), ("blk_qmax", i32), ("ctx_cap", i32)]
 
 
+WS_FIELDS = ("x", "h", "attn", "q", "img", "ascale", "part", "counters", "arg_val", "arg_idx", "att_o", "att_ml")
+
+
 class Workspace(C.Structure):
-    _fields_ = [(n, vp) for n in ("x", "h", "attn", "q", "img", "ascale", "part", "counters",
-                                  "arg_val", "arg_idx")]
+    _fields_ = [(n, vp) for n in WS_FIELDS]
 
 
 class WorkspaceSizes(C.Structure):
-    _fields_ = [(n, C.c_size_t) for n in ("x", "h", "attn", "q", "img", "ascale", "part", "counters",
-                                          "arg_val", "arg_idx")]
+    _fields_ = [(n, C.c_size_t) for n in WS_FIELDS]
 
 
 class Seq(C.Structure):
@@ -76,7 +77,12 @@ _SIGS = {
     "qs_act_quant": ([vp, i32, i32, i32, vp, vp, vp, vp], C.c_int),
     "qs_w4a4_linear": ([C.POINTER(QWeight), vp, i32, vp, C.POINTER(Workspace), vp], C.c_int),
     "qs_w4a16_linear": ([C.POINTER(QWeight), vp, i32, vp, C.POINTER(Workspace), vp], C.c_int),
+    "qs_linear_prepacked": ([C.POINTER(QWeight), i32, i32, vp, C.POINTER(Workspace), vp], C.c_int),
+    "qs_debug_timeline": ([vp], C.c_int),
     "qs_linear_group_dots": ([C.POINTER(QWeight), vp, i32, i32, vp, C.POINTER(Workspace), vp], C.c_int),
+    "qs_profile_enable": ([i32], C.c_int),
+    "qs_profile_reset": ([], C.c_int),
+    "qs_profile_read": ([vp, vp, i32, C.POINTER(i32)], C.c_int),
     "qs_forward": ([C.POINTER(Model), C.POINTER(Batch), i32, C.POINTER(Workspace), vp, vp, vp], C.c_int),
     "qs_draft_prep": ([C.POINTER(Seq), i32, vp], C.c_int),
     "qs_verify_prep": ([C.POINTER(Seq), vp], C.c_int),

@@ -1,7 +1,7 @@
 // W4A4 (draft) / W4A16 (verify) quantised linear on 5th-gen tensor cores.
 //
-// y[t, n] = sum_g  wscale[g, n] * ascale[g, t] * D[t, n, g]
-// D[t, n, g] = sum_{k in g} code_w[n, k] * X[t, k]       (exact int32 on tcgen05 kind::i8)
+// y[t, n] = sum_c  wscale[n, c] * ascale[c, t] * D[t, n, c]       (c = 128-wide K chunk)
+// D[t, n, c] = sum_{k in c} code_w[n, k] * X[t, k]                 (exact int32, tcgen05 kind::i8)
 //
 //   draft  (L=1): X = int4 activation codes of the reference's per-(token, group)
 //                 quantiser (quant.py:179-194); ascale = its scale.
@@ -10,13 +10,22 @@
 //                 columns; ascale = 2^-e.  Same weights, same kernel, same
 //                 tensor-core instruction -- only the B operand changes.
 //
-// Persistent, warp-specialised, stream-K over (tile, group) units:
-//   warp 0      producer: bulk-async copies of packed weight chunks + activation image
-//   warp 1      MMA issuer (one thread): tcgen05.mma.kind::i8, A from TMEM, B from smem
+// Persistent, warp-specialised, stream-K over (tile, chunk) units.  Units are
+// processed in STAGES of up to CPS consecutive chunks of one tile so that every
+// synchronisation (mbarrier wait / arrive / commit, bulk-copy issue -- each
+// ~100 ns of latency on its issuing thread) is amortised over CPS x 8 KiB of
+// weights:
+//   warp 0      producer: one bulk copy of the stage's packed weights (CPS x 8 KiB,
+//               contiguous) + one of its activation image
+//   warp 1      MMA issuer (one thread): tcgen05.mma.kind::i8, A = weights in TMEM,
+//               B = activation image in smem (128B swizzle), D = int32 in TMEM,
+//               one accumulator column block per chunk of the stage
 //   warp 2      TMEM allocator
+//   warp 3      scale producer: per-stage bulk copies of weight / activation scales
 //   warps 4-7   unpack: packed int4 (smem) -> int8 (registers) -> TMEM A operand
-//   warps 8-11  epilogue: per-group TMEM drain, fp32 scale-accumulate, stream-K
-//               fixup (fixed order => deterministic), fused post-op.
+//   warps 8-15  epilogue (2 per TMEM lane quadrant, token chunks split): per-chunk
+//               TMEM drain, fp32 scale-accumulate, stream-K fixup (fixed order =>
+//               deterministic), fused post-op.
 // The reduction order of every output depends only on (N, K, grid), never on T,
 // so an n-token call is bit-identical to n single-token calls.
 #include "ptx.cuh"
@@ -27,16 +36,24 @@ namespace qs {
 template <int L, int TMAX>
 struct LinCfg {
   static constexpr int kRowsMax = (L * TMAX) <= 8 ? 8 : ((L * TMAX + 15) / 16) * 16;
-  static constexpr int kActBytes = kRowsMax * 128;
-  static constexpr int kStageBytes = kChunkBytes + kActBytes;
-  static constexpr int kStages = (200 * 1024 / kStageBytes) > 10 ? 10 : (200 * 1024 / kStageBytes);
-  static constexpr int kTStages = 4;                 // TMEM A-operand slots (32 cols each)
-  static constexpr int kAccCols = kRowsMax < 32 ? 32 : kRowsMax;
-  static constexpr int kAColBase = 2 * kAccCols;
+  static constexpr int kAccCols = ((kRowsMax + 31) / 32) * 32;  // one accumulator block per chunk
+  // chunks per stage: as many as TMEM allows (2 acc buffers + 2 A slots)
+  static constexpr int kCPS = (2 * 4 * kAccCols + 2 * 4 * 32 <= 512) ? 4
+                              : (2 * 2 * kAccCols + 2 * 2 * 32 <= 512) ? 2 : 1;
+  static constexpr int kAColBase = 2 * kCPS * kAccCols;
   static constexpr int kTmemCols = 512;
-  static_assert(2 * kAccCols + kTStages * 32 <= kTmemCols, "TMEM budget");
-  static constexpr int kBarOff = kStages * kStageBytes;
-  static constexpr int kNumBars = 2 * kStages + 2 * kTStages + 4;
+  static_assert(kAColBase + 2 * kCPS * 32 <= kTmemCols, "TMEM budget");
+  static constexpr int kActBytes = kRowsMax * 128;
+  static constexpr int kStageBytes = kCPS * (kChunkBytes + kActBytes);
+  static constexpr int kStages0 = (196 * 1024) / kStageBytes;
+  static constexpr int kStages = kStages0 > 8 ? 8 : kStages0;
+  static_assert(kStages >= 2, "pipeline depth");
+  static constexpr int kSStages = kStages + 2;
+  static constexpr int kSEntry = kCPS * (128 + TMAX) * 4;
+  static constexpr int kOwnChunks = (TMAX / 8 + 1) / 2;  // token chunks per epilogue half
+  static constexpr int kScaleOff = kStages * kStageBytes;
+  static constexpr int kBarOff = kScaleOff + kSStages * kSEntry;
+  static constexpr int kNumBars = 2 * kStages + 4 + 4 + 2 * kSStages;
   static constexpr int kSmemBytes = kBarOff + kNumBars * 8 + 16 + 4 * TMAX * 8 + 1024;
 };
 
@@ -46,7 +63,7 @@ __device__ __forceinline__ uint32_t sext_nib(uint32_t n) {  // 4 nibbles (one pe
 
 __device__ __forceinline__ long long umul_div(long long a, long long b, long long c) { return a * b / c; }
 
-// CTA c of P covers units [bnd(c), bnd(c+1)) of U = n_tiles * G.
+// CTA c of P covers units [bnd(c), bnd(c+1)) of U = n_tiles * n_chunks.
 __device__ __forceinline__ int unit_bound(int c, int U, int P) { return (int)umul_div(c, U, P); }
 __device__ __forceinline__ int cta_of_unit(int u, int U, int P) {
   int c = (int)umul_div(u, P, U);
@@ -60,31 +77,61 @@ __device__ __forceinline__ float silu_ref(float g) {
   return __fdiv_rn(g, __fadd_rn(1.0f, expf(-g)));
 }
 
+// Stage iterator shared by every role: runs of <= CPS chunks of one tile.
+struct StageIt {
+  int u, u1, NC, cps;
+  int tile, ch0, nq;
+  __device__ __forceinline__ bool next() {
+    if (u >= u1) return false;
+    tile = u / NC;
+    ch0 = u - tile * NC;
+    int end = u + cps;
+    const int tile_end = (tile + 1) * NC;
+    if (end > tile_end) end = tile_end;
+    if (end > u1) end = u1;
+    nq = end - u;
+    u = end;
+    return true;
+  }
+};
+
 template <int L, int TMAX>
-__global__ void __launch_bounds__(384, 1) linear_tc_kernel(const LinearArgs a) {
+__global__ void __launch_bounds__(512, 1) linear_tc_kernel(const LinearArgs a) {
   using C = LinCfg<L, TMAX>;
+  constexpr int CPS = C::kCPS;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kBarOff);
-  uint64_t* full = bars;                       // [kStages] producer -> MMA/unpack (tx bytes)
-  uint64_t* empty = bars + C::kStages;         // [kStages] MMA commit -> producer
-  uint64_t* tfull = empty + C::kStages;        // [kTStages] unpack -> MMA
-  uint64_t* tempty = tfull + C::kTStages;      // [kTStages] MMA commit -> unpack
-  uint64_t* accfull = tempty + C::kTStages;    // [2] MMA commit -> epilogue
+  uint64_t* full = bars;                       // [kStages] weights+act landed (tx bytes)
+  uint64_t* empty = full + C::kStages;         // [kStages] MMA commit -> producer
+  uint64_t* tfull = empty + C::kStages;        // [2] unpack -> MMA
+  uint64_t* tempty = tfull + 2;                // [2] MMA commit -> unpack
+  uint64_t* accfull = tempty + 2;              // [2] MMA commit -> epilogue
   uint64_t* accempty = accfull + 2;            // [2] epilogue -> MMA
+  uint64_t* sfull = accempty + 2;              // [kSStages] scales landed
+  uint64_t* sempty = sfull + C::kSStages;      // [kSStages] epilogue -> scale producer
+  float* sring = reinterpret_cast<float*>(smem + C::kScaleOff);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::kNumBars);
   int* flag = reinterpret_cast<int*>(tmem_slot + 2);
   float* red_val = reinterpret_cast<float*>(tmem_slot + 4);  // [4][TMAX]
   int* red_idx = reinterpret_cast<int*>(red_val + 4 * TMAX);  // [4][TMAX]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int U = a.n_tiles * a.G, P = a.n_cta, c = blockIdx.x;
+  const int NC = a.n_chunks;
+  const int U = a.n_tiles * NC, P = a.n_cta, c = blockIdx.x;
   const int u0 = unit_bound(c, U, P), u1 = unit_bound(c + 1, U, P);
+  const bool dbg0 = a.dbg != nullptr && c == 0;
+  if (a.dbg && threadIdx.x == 0) a.dbg[1024 + c] = gtimer();
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < C::kStages; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
-    for (int i = 0; i < C::kTStages; ++i) { mbar_init(&tfull[i], 4); mbar_init(&tempty[i], 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(&accfull[i], 1); mbar_init(&accempty[i], 4); }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 4);
+      mbar_init(&tempty[i], 1);
+      mbar_init(&accfull[i], 1);
+      mbar_init(&accempty[i], 8);
+    }
+    for (int i = 0; i < C::kSStages; ++i) { mbar_init(&sfull[i], 1); mbar_init(&sempty[i], 8); }
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc<C::kTmemCols>(tmem_slot);
@@ -92,238 +139,299 @@ __global__ void __launch_bounds__(384, 1) linear_tc_kernel(const LinearArgs a) {
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const int cpg = a.cpg;
   const uint32_t act_bytes = (uint32_t)a.r_pad * 128u;
 
   if (warp == 0) {
-    // ------------------------------------------------------------ producer
-    if (lane == 0) {
-      int i = 0;
-      for (int u = u0; u < u1; ++u) {
-        const int tile = u / a.G, gi = u % a.G;
-        for (int cc = 0; cc < cpg; ++cc, ++i) {
-          const int ch = gi * cpg + cc, s = i % C::kStages;
-          mbar_wait(&empty[s], ((i / C::kStages) & 1) ^ 1);
-          uint8_t* st = smem + s * C::kStageBytes;
-          mbar_arrive_expect_tx(&full[s], kChunkBytes + act_bytes);
-          bulk_g2s(st, a.codes + ((size_t)tile * a.n_chunks + ch) * kChunkBytes, kChunkBytes, &full[s]);
-          bulk_g2s(st + kChunkBytes, a.act + (size_t)ch * act_bytes, act_bytes, &full[s]);
-        }
+    // ------------------------------------------------------------ weight/act producer (warp-wide, elected issue)
+    {
+      StageIt it{u0, u1, NC, CPS};
+      for (int i = 0; it.next(); ++i) {
+        const int s = i % C::kStages;
+        mbar_wait(&empty[s], ((i / C::kStages) & 1) ^ 1);
+        uint8_t* st = smem + s * C::kStageBytes;
+        mbar_arrive_expect_tx_elect(&full[s], (uint32_t)it.nq * (kChunkBytes + act_bytes));
+        bulk_g2s_elect(st, a.codes + ((size_t)it.tile * NC + it.ch0) * kChunkBytes, it.nq * kChunkBytes, &full[s]);
+        bulk_g2s_elect(st + CPS * kChunkBytes, a.act + (size_t)it.ch0 * act_bytes, it.nq * act_bytes, &full[s]);
+        if (dbg0 && i < 64 && lane == 0) a.dbg[0 * 64 + i] = gtimer();
+      }
+    }
+  } else if (warp == 3) {
+    // ------------------------------------------------------------ scale producer (warp-wide, elected issue)
+    {
+      const uint32_t a_bytes = (uint32_t)a.a_ld * 4u;
+      StageIt it{u0, u1, NC, CPS};
+      for (int i = 0; it.next(); ++i) {
+        const int ss = i % C::kSStages;
+        mbar_wait(&sempty[ss], ((i / C::kSStages) & 1) ^ 1);
+        float* se = sring + ss * (C::kSEntry / 4);
+        mbar_arrive_expect_tx_elect(&sfull[ss], (uint32_t)it.nq * (512u + a_bytes));
+        bulk_g2s_elect(se, a.wscale + ((size_t)it.tile * NC + it.ch0) * kTileN, it.nq * 512u, &sfull[ss]);
+        bulk_g2s_elect(se + CPS * 128, a.ascale + (size_t)it.ch0 * a.a_ld, it.nq * a_bytes, &sfull[ss]);
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
+    // ------------------------------------------------------------ MMA issuer (warp-wide, elected issue)
+    {
       const uint32_t idesc = idesc_i8(128, (uint32_t)a.r_pad);
-      int i = 0, j = 0;
-      for (int u = u0; u < u1; ++u, ++j) {
-        const int b = j & 1;
-        mbar_wait(&accempty[b], ((j >> 1) & 1) ^ 1);
+      StageIt it{u0, u1, NC, CPS};
+      for (int i = 0; it.next(); ++i) {
+        const int s = i % C::kStages, b = i & 1;
+        if (dbg0 && i < 64 && lane == 0) a.dbg[4 * 64 + i] = gtimer();
+        mbar_wait(&accempty[b], ((i >> 1) & 1) ^ 1);
+        if (dbg0 && i < 64 && lane == 0) a.dbg[5 * 64 + i] = gtimer();
+        mbar_wait(&full[s], (i / C::kStages) & 1);
+        if (dbg0 && i < 64 && lane == 0) a.dbg[6 * 64 + i] = gtimer();
+        mbar_wait(&tfull[b], (i >> 1) & 1);
         tc_fence_after();
-        const uint32_t d_tmem = tmem + b * C::kAccCols;
-        for (int cc = 0; cc < cpg; ++cc, ++i) {
-          const int s = i % C::kStages, ts = i % C::kTStages;
-          mbar_wait(&full[s], (i / C::kStages) & 1);
-          mbar_wait(&tfull[ts], (i / C::kTStages) & 1);
-          tc_fence_after();
-          const uint32_t b_base = smem_u32(smem + s * C::kStageBytes + kChunkBytes);
-          const uint32_t a_tmem = tmem + C::kAColBase + ts * 32;
+        if (dbg0 && i < 64 && lane == 0) a.dbg[7 * 64 + i] = gtimer();
+        const uint32_t b_base = smem_u32(smem + s * C::kStageBytes + CPS * kChunkBytes);
+        for (int q = 0; q < it.nq; ++q) {
+          const uint32_t d_tmem = tmem + (b * CPS + q) * C::kAccCols;
+          const uint32_t a_tmem = tmem + C::kAColBase + (b * CPS + q) * 32;
+          const uint32_t bq = b_base + q * act_bytes;
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
-            mma_i8_ts(d_tmem, a_tmem + kk * 8, sdesc_sw128(b_base + kk * 32), idesc, (cc | kk) != 0);
-          }
-          mma_commit(&empty[s]);
-          mma_commit(&tempty[ts]);
+          for (int kk = 0; kk < 4; ++kk)
+            mma_i8_ts_elect(d_tmem, a_tmem + kk * 8, sdesc_sw128(bq + kk * 32), idesc, kk);
         }
-        mma_commit(&accfull[b]);
+        if (dbg0 && i < 64 && lane == 0) a.dbg[8 * 64 + i] = gtimer();
+        mma_commit_elect(&empty[s]);
+        mma_commit_elect(&tempty[b]);
+        mma_commit_elect(&accfull[b]);
+        if (dbg0 && i < 64 && lane == 0) a.dbg[2 * 64 + i] = gtimer();
       }
     }
   } else if (warp >= 4 && warp < 8) {
     // ------------------------------------------------------------ unpack
-    const int q = warp & 3, r = q * 32 + lane;
-    const uint32_t lane_base = (uint32_t)(q * 32) << 16;
-    int i = 0;
-    for (int u = u0; u < u1; ++u) {
-      for (int cc = 0; cc < cpg; ++cc, ++i) {
-        const int s = i % C::kStages, ts = i % C::kTStages;
-        mbar_wait(&full[s], (i / C::kStages) & 1);
-        mbar_wait(&tempty[ts], ((i / C::kTStages) & 1) ^ 1);
-        tc_fence_after();
-        const uint4* src = reinterpret_cast<const uint4*>(smem + s * C::kStageBytes);
-        uint32_t v[32];
+    const int q4 = warp & 3, r = q4 * 32 + lane;
+    const uint32_t lane_base = (uint32_t)(q4 * 32) << 16;
+    StageIt it{u0, u1, NC, CPS};
+    for (int i = 0; it.next(); ++i) {
+      const int s = i % C::kStages, b = i & 1;
+      mbar_wait_warp(&full[s], (i / C::kStages) & 1, 20);
+      mbar_wait_warp(&tempty[b], ((i >> 1) & 1) ^ 1, 20);
+      tc_fence_after();
+      if (dbg0 && i < 64 && r == 0) a.dbg[9 * 64 + i] = gtimer();
+      // all LDS of the stage first (latency overlap), then unpack + TMEM stores
+      uint4 wv[CPS][4];
 #pragma unroll
-        for (int jp = 0; jp < 4; ++jp) {
-          const uint4 w = src[jp * 128 + r];
-          const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+      for (int q = 0; q < CPS; ++q) {
+        if (q < it.nq) {
+          const uint4* src = reinterpret_cast<const uint4*>(smem + s * C::kStageBytes + q * kChunkBytes);
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int m = jp * 4 + e;
-            v[m] = sext_nib(ww[e] & 0x0F0F0F0Fu);
-            v[16 + m] = sext_nib((ww[e] >> 4) & 0x0F0F0F0Fu);
-          }
+          for (int jp = 0; jp < 4; ++jp) wv[q][jp] = src[jp * 128 + r];
         }
-        tmem_st32(tmem + lane_base + C::kAColBase + ts * 32, v);
-        tmem_wait_st();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&tfull[ts]);
       }
+#pragma unroll
+      for (int q = 0; q < CPS; ++q) {
+        if (q < it.nq) {
+          uint32_t v[32];
+#pragma unroll
+          for (int jp = 0; jp < 4; ++jp) {
+            const uint32_t ww[4] = {wv[q][jp].x, wv[q][jp].y, wv[q][jp].z, wv[q][jp].w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int m = jp * 4 + e;
+              v[m] = sext_nib(ww[e] & 0x0F0F0F0Fu);
+              v[16 + m] = sext_nib((ww[e] >> 4) & 0x0F0F0F0Fu);
+            }
+          }
+          tmem_st32(tmem + lane_base + C::kAColBase + (b * CPS + q) * 32, v);
+        }
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tfull[b]);
+      if (dbg0 && i < 64 && r == 0) a.dbg[1 * 64 + i] = gtimer();
     }
   } else if (warp >= 8) {
     // ------------------------------------------------------------ epilogue
-    const int q = warp & 3, r = q * 32 + lane, et = threadIdx.x - 256;
-    const uint32_t lane_base = (uint32_t)(q * 32) << 16;
-    float acc[TMAX];
+    // lane quadrant q4 = warp & 3 (TMEM lanes 32q4.. = tile rows); half h owns the
+    // token chunks tc with (tc & 1) == h.
+    const int q4 = warp & 3, h = (warp - 8) >> 2, r = q4 * 32 + lane, et = threadIdx.x - 256;
+    const uint32_t lane_base = (uint32_t)(q4 * 32) << 16;
+    constexpr int kOwn = C::kOwnChunks;
+    float acc[kOwn * 8];
 #pragma unroll
-    for (int t = 0; t < TMAX; ++t) acc[t] = 0.f;
-    int j = 0;
-    for (int u = u0; u < u1; ++u, ++j) {
-      const int tile = u / a.G, gi = u % a.G, b = j & 1;
-      const int n = tile * kTileN + r;
-      const float sw = a.wscale[(size_t)gi * a.n_pad + n];
-      const float* asc = a.ascale + (size_t)gi * a.a_ld;
-      mbar_wait(&accfull[b], (j >> 1) & 1);
+    for (int t = 0; t < kOwn * 8; ++t) acc[t] = 0.f;
+    StageIt it{u0, u1, NC, CPS};
+    for (int i = 0; it.next(); ++i) {
+      const int b = i & 1, ss = i % C::kSStages;
+      const int tile = it.tile, n = tile * kTileN + r;
+      mbar_wait_warp(&sfull[ss], (i / C::kSStages) & 1, 64);
+      mbar_wait_warp(&accfull[b], (i >> 1) & 1, 64);
       tc_fence_after();
-      const uint32_t col0 = tmem + lane_base + b * C::kAccCols;
+      if (dbg0 && i < 64 && et == 0) a.dbg[10 * 64 + i] = gtimer();
+      const float* se = sring + ss * (C::kSEntry / 4);
       if (a.op == kOpDump) {
-        for (int c0 = 0; c0 < a.r_pad; c0 += 8) {
-          uint32_t rr[8];
-          tmem_ld8(col0 + c0, rr);
-          tmem_wait_ld();
-          for (int e = 0; e < 8; ++e)
-            a.dump[((size_t)n * a.G + gi) * a.r_pad + c0 + e] = (int32_t)rr[e];
+        if (h == 0) {
+          for (int q = 0; q < it.nq; ++q) {
+            const uint32_t col0 = tmem + lane_base + (b * CPS + q) * C::kAccCols;
+            const int ch = it.ch0 + q;
+            for (int c0 = 0; c0 < a.r_pad; c0 += 8) {
+              uint32_t rr[8];
+              tmem_ld8(col0 + c0, rr);
+              tmem_wait_ld();
+              for (int e = 0; e < 8; ++e) a.dump[((size_t)n * NC + ch) * a.r_pad + c0 + e] = (int32_t)rr[e];
+            }
+          }
         }
       } else {
+        float sw[CPS];
 #pragma unroll
-        for (int tc = 0; tc < TMAX / 8; ++tc) {
+        for (int q = 0; q < CPS; ++q) sw[q] = (q < it.nq) ? se[q * 128 + r] : 0.f;
+#pragma unroll
+        for (int lc = 0; lc < kOwn; ++lc) {
+          const int tc = 2 * lc + h;
           if (tc * 8 < a.T) {
-            uint32_t rr[L][8];
+            // one TMEM round trip per token chunk for all chunks of the stage
+            uint32_t rr[CPS][8 * L];
 #pragma unroll
-            for (int l = 0; l < L; ++l) tmem_ld8(col0 + tc * 8 * L + l * 8, rr[l]);
-            tmem_wait_ld();
-            const float4 s0 = *reinterpret_cast<const float4*>(asc + tc * 8);
-            const float4 s1 = *reinterpret_cast<const float4*>(asc + tc * 8 + 4);
-            const float as[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              float dv;
-              if constexpr (L == 1) {
-                dv = (float)(int32_t)rr[0][e];
-              } else {
-                // column order within the 24-column block: token-major, limb-minor
-                const int cidx = e * 3;
-                const int32_t d0 = (int32_t)rr[(cidx + 0) / 8][(cidx + 0) % 8];
-                const int32_t d1 = (int32_t)rr[(cidx + 1) / 8][(cidx + 1) % 8];
-                const int32_t d2 = (int32_t)rr[(cidx + 2) / 8][(cidx + 2) % 8];
-                const long long dd = ((long long)d2 << 16) + ((long long)d1 << 8) + (long long)d0;
-                dv = (float)dd;
+            for (int q = 0; q < CPS; ++q) {
+              if (q < it.nq) {
+                const uint32_t col0 = tmem + lane_base + (b * CPS + q) * C::kAccCols;
+                if constexpr (L == 1) {
+                  tmem_ld8(col0 + tc * 8, *reinterpret_cast<uint32_t(*)[8]>(rr[q]));
+                } else {
+                  tmem_ld16(col0 + tc * 24, rr[q]);
+                  tmem_ld8(col0 + tc * 24 + 16, *reinterpret_cast<uint32_t(*)[8]>(rr[q] + 16));
+                }
               }
-              acc[tc * 8 + e] = __fadd_rn(acc[tc * 8 + e], __fmul_rn(dv, __fmul_rn(sw, as[e])));
+            }
+            tmem_wait_ld();
+#pragma unroll
+            for (int q = 0; q < CPS; ++q) {
+              if (q < it.nq) {
+                const float* asc = se + CPS * 128 + q * a.a_ld;
+                const float4 s0 = *reinterpret_cast<const float4*>(asc + tc * 8);
+                const float4 s1 = *reinterpret_cast<const float4*>(asc + tc * 8 + 4);
+                const float as[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                  float dv;
+                  if constexpr (L == 1) {
+                    dv = (float)(int32_t)rr[q][e];
+                  } else {
+                    // token-major, limb-minor columns: X = l2*2^16 + l1*2^8 + l0.
+                    // d1*256+d0 is exact in int32; one rounding in the fma.
+                    const int32_t lo = (int32_t)rr[q][3 * e + 1] * 256 + (int32_t)rr[q][3 * e];
+                    dv = fmaf((float)(int32_t)rr[q][3 * e + 2], 65536.0f, (float)lo);
+                  }
+                  acc[lc * 8 + e] = fmaf(dv, sw[q] * as[e], acc[lc * 8 + e]);
+                }
+              }
             }
           }
         }
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&accempty[b]);
+      if (lane == 0) {
+        mbar_arrive(&accempty[b]);
+        mbar_arrive(&sempty[ss]);
+      }
+      if (dbg0 && i < 64 && et == 0) a.dbg[3 * 64 + i] = gtimer();
 
-      // ---- segment end: stream-K fixup + post-op
-      const bool seg_end = (gi == a.G - 1) || (u == u1 - 1);
+      // ---- segment end (stages never straddle tiles): stream-K fixup + post-op
+      const int last_u = tile * NC + it.ch0 + it.nq - 1;
+      const bool seg_end = (it.ch0 + it.nq == NC) || (last_u == u1 - 1);
       if (!seg_end || a.op == kOpDump) continue;
-      const int c_lo = cta_of_unit(tile * a.G, U, P);
-      const int c_hi = cta_of_unit(tile * a.G + a.G - 1, U, P);
+      const int c_lo = cta_of_unit(tile * NC, U, P);
+      const int c_hi = cta_of_unit(tile * NC + NC - 1, U, P);
       if (c_hi > c_lo) {
         float* my = a.part + ((size_t)(c + tile) * TMAX) * kTileN;
 #pragma unroll
-        for (int t = 0; t < TMAX; ++t)
-          if (t < a.T) my[t * kTileN + r] = acc[t];
+        for (int lc = 0; lc < kOwn; ++lc)
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const int t = (2 * lc + h) * 8 + e;
+            if (t < a.T) my[t * kTileN + r] = acc[lc * 8 + e];
+          }
         __threadfence();
-        named_bar(1, 128);
+        named_bar(1, 256);
         if (et == 0) {
           const int old = atomicAdd(&a.counters[tile], 1);
           *flag = (old == c_hi - c_lo);
         }
-        named_bar(1, 128);
+        named_bar(1, 256);
         const int last = *flag;
-        named_bar(1, 128);
-        if (!last) {
+        named_bar(1, 256);
 #pragma unroll
-          for (int t = 0; t < TMAX; ++t) acc[t] = 0.f;
-          continue;
-        }
+        for (int t = 0; t < kOwn * 8; ++t) acc[t] = 0.f;
+        if (!last) continue;
         __threadfence();
-#pragma unroll
-        for (int t = 0; t < TMAX; ++t) acc[t] = 0.f;
         for (int cc2 = c_lo; cc2 <= c_hi; ++cc2) {
           const volatile float* pp = a.part + ((size_t)(cc2 + tile) * TMAX) * kTileN;
 #pragma unroll
-          for (int t = 0; t < TMAX; ++t)
-            if (t < a.T) acc[t] = __fadd_rn(acc[t], pp[t * kTileN + r]);
+          for (int lc = 0; lc < kOwn; ++lc)
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const int t = (2 * lc + h) * 8 + e;
+              if (t < a.T) acc[lc * 8 + e] = __fadd_rn(acc[lc * 8 + e], pp[t * kTileN + r]);
+            }
         }
         if (et == 0) a.counters[tile] = 0;
       }
       // ---------------------------------------------------------- post-ops
       const bool valid = n < a.n;
-      if (a.op == kOpStore || a.op == kOpResidual) {
 #pragma unroll
-        for (int t = 0; t < TMAX; ++t) {
-          if (t < a.T && valid) {
-            float* o = a.out + (size_t)t * a.ldo + n;
-            *o = (a.op == kOpResidual) ? __fadd_rn(*o, acc[t]) : acc[t];
+      for (int lc = 0; lc < kOwn; ++lc) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const int t = (2 * lc + h) * 8 + e;
+          const float v = acc[lc * 8 + e];
+          if (a.op == kOpStore || a.op == kOpResidual) {
+            if (t < a.T && valid) {
+              float* o = a.out + (size_t)t * a.ldo + n;
+              *o = (a.op == kOpResidual) ? __fadd_rn(*o, v) : v;
+            }
+          } else if (a.op == kOpSiluMul) {
+            const float other = __shfl_xor_sync(0xffffffffu, v, 1);
+            if (t < a.T && valid && (r & 1) == 0)
+              a.out[(size_t)t * a.ldo + (n >> 1)] = __fmul_rn(silu_ref(v), other);
+          } else if (a.op == kOpQkvRope) {
+            const float other = __shfl_xor_sync(0xffffffffu, v, 1);
+            if (t < a.T && valid) {
+              const bool is_v = n >= a.n_q + a.n_k;
+              const int loc = n < a.n_q ? n : (is_v ? n - a.n_q - a.n_k : n - a.n_q);
+              const int d = loc % a.hd, head = loc / a.hd, half = a.hd >> 1, ip = d >> 1;
+              const bool odd = (d & 1) != 0;
+              const int p = a.pos[t];
+              float val = v;
+              if (!is_v) {
+                // model.py:243-252: even' = e*c - o*s ; odd' = e*s + o*c
+                const float cs = a.rope_cos[(size_t)p * half + ip], sn = a.rope_sin[(size_t)p * half + ip];
+                const float ev = odd ? other : v, ov = odd ? v : other;
+                val = odd ? __fadd_rn(__fmul_rn(ev, sn), __fmul_rn(ov, cs))
+                          : __fsub_rn(__fmul_rn(ev, cs), __fmul_rn(ov, sn));
+              }
+              if (n < a.n_q) {
+                a.out[(size_t)t * a.ldo + n] = val;
+              } else {
+                const int sl = a.slot[t];
+                const int pg = a.block_table[(size_t)sl * a.bt_ld + p / a.page];
+                const size_t off = (((size_t)pg * a.n_kv_heads + head) * a.page + (p % a.page)) * a.hd + d;
+                (is_v ? a.vcache : a.kcache)[off] = val;
+              }
+            }
+          } else if (a.op == kOpLogits) {
+            if (t < a.T) {
+              if (a.out != nullptr && valid) a.out[(size_t)t * a.ldo + n] = v;
+              float bv = valid ? v : -INFINITY;
+              int bi = valid ? n : 0x7fffffff;
+#pragma unroll
+              for (int off = 16; off > 0; off >>= 1) {
+                const float ov = __shfl_xor_sync(0xffffffffu, bv, off);
+                const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+                if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+              }
+              if (lane == 0) { red_val[q4 * TMAX + t] = bv; red_idx[q4 * TMAX + t] = bi; }
+            }
           }
         }
-      } else if (a.op == kOpSiluMul) {
-#pragma unroll
-        for (int t = 0; t < TMAX; ++t) {
-          const float other = __shfl_xor_sync(0xffffffffu, acc[t], 1);
-          if (t < a.T && valid && (r & 1) == 0)
-            a.out[(size_t)t * a.ldo + (n >> 1)] = __fmul_rn(silu_ref(acc[t]), other);
-        }
-      } else if (a.op == kOpQkvRope) {
-        const bool is_v = n >= a.n_q + a.n_k;
-        const int loc = n < a.n_q ? n : (is_v ? n - a.n_q - a.n_k : n - a.n_q);
-        const int d = loc % a.hd, head = loc / a.hd, half = a.hd >> 1, ip = d >> 1;
-        const bool odd = (d & 1) != 0;
-#pragma unroll
-        for (int t = 0; t < TMAX; ++t) {
-          const float other = __shfl_xor_sync(0xffffffffu, acc[t], 1);
-          if (t < a.T && valid) {
-            const int p = a.pos[t];
-            float val = acc[t];
-            if (!is_v) {
-              // model.py:243-252: even' = e*c - o*s ; odd' = e*s + o*c
-              const float cs = a.rope_cos[(size_t)p * half + ip], sn = a.rope_sin[(size_t)p * half + ip];
-              const float e = odd ? other : acc[t], o = odd ? acc[t] : other;
-              val = odd ? __fadd_rn(__fmul_rn(e, sn), __fmul_rn(o, cs)) : __fsub_rn(__fmul_rn(e, cs), __fmul_rn(o, sn));
-            }
-            if (n < a.n_q) {
-              a.out[(size_t)t * a.ldo + n] = val;
-            } else {
-              const int sl = a.slot[t];
-              const int pg = a.block_table[(size_t)sl * a.bt_ld + p / a.page];
-              const size_t off = (((size_t)pg * a.n_kv_heads + head) * a.page + (p % a.page)) * a.hd + d;
-              (is_v ? a.vcache : a.kcache)[off] = val;
-            }
-          }
-        }
-      } else if (a.op == kOpLogits) {
-        // store logits, then first-index argmax over this tile, then over tiles
-#pragma unroll
-        for (int t = 0; t < TMAX; ++t) {
-          if (t < a.T) {
-            if (a.out != nullptr && valid) a.out[(size_t)t * a.ldo + n] = acc[t];
-            float bv = valid ? acc[t] : -INFINITY;
-            int bi = valid ? n : 0x7fffffff;
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) {
-              const float ov = __shfl_xor_sync(0xffffffffu, bv, off);
-              const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
-              if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
-            }
-            if (lane == 0) { red_val[q * TMAX + t] = bv; red_idx[q * TMAX + t] = bi; }
-          }
-        }
-        named_bar(1, 128);
+      }
+      if (a.op == kOpLogits) {
+        named_bar(1, 256);
         if (et < a.T) {
           float bv = red_val[et];
           int bi = red_idx[et];
@@ -336,14 +444,14 @@ __global__ void __launch_bounds__(384, 1) linear_tc_kernel(const LinearArgs a) {
           a.arg_idx[(size_t)tile * TMAX + et] = bi;
         }
         __threadfence();
-        named_bar(1, 128);
+        named_bar(1, 256);
         if (et == 0) {
           const int old = atomicAdd(&a.counters[a.n_tiles], 1);
           *flag = (old == a.n_tiles - 1);
         }
-        named_bar(1, 128);
+        named_bar(1, 256);
         const int last = *flag;
-        named_bar(1, 128);
+        named_bar(1, 256);
         if (last) {
           __threadfence();
           if (et < a.T) {
@@ -362,7 +470,7 @@ __global__ void __launch_bounds__(384, 1) linear_tc_kernel(const LinearArgs a) {
         }
       }
 #pragma unroll
-      for (int t = 0; t < TMAX; ++t) acc[t] = 0.f;
+      for (int t = 0; t < kOwn * 8; ++t) acc[t] = 0.f;
     }
   }
   tc_fence_before();
@@ -371,6 +479,7 @@ __global__ void __launch_bounds__(384, 1) linear_tc_kernel(const LinearArgs a) {
     tc_fence_after();
     tmem_dealloc<C::kTmemCols>(tmem);
   }
+  if (a.dbg && threadIdx.x == 0) a.dbg[2048 + c] = gtimer();
 }
 
 template <int L, int TMAX>
@@ -383,7 +492,7 @@ static cudaError_t launch_linear_t(const LinearArgs& a, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  linear_tc_kernel<L, TMAX><<<a.n_cta, 384, C::kSmemBytes, st>>>(a);
+  linear_tc_kernel<L, TMAX><<<a.n_cta, 512, C::kSmemBytes, st>>>(a);
   return cudaGetLastError();
 }
 

@@ -70,6 +70,9 @@ struct LinearArgs {
   int* argmax_out;
   // kOpDump
   int32_t* dump;
+  // debug timeline (CTA 0): [role][i] globaltimer ns; roles: 0 producer issue, 1 unpack done,
+  // 2 mma issued, 3 epilogue start (acc ready), 4 epilogue done
+  unsigned long long* dbg;
 };
 
 struct PackArgs {
@@ -87,11 +90,19 @@ struct PackArgs {
   float* scales_out;
   float* fq_out;
   float* y_out;
+  // attention combine mode (o_proj operand): x[t, h*hd+d] = sum_c w_c o_c[d] / sum_c w_c l_c
+  const float* att_o;   // [T][H][cmax][hd]
+  const float* att_ml;  // [T][H][cmax][2]  (chunk max, chunk sum)
+  const int* att_pos;   // [T] query positions (context = pos + 1)
+  int att_hd, att_cmax, att_chunk;
 };
 
 struct AttnArgs {
   const float* q;
   int ldq;
+  float* part_o;   // [T][H][cmax][hd] split-KV partials
+  float* part_ml;  // [T][H][cmax][2]
+  int cmax;        // chunks per query capacity
   const float* kcache;
   const float* vcache;
   const int* block_table;

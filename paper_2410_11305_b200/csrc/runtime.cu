@@ -14,6 +14,8 @@ cudaError_t launch_linear(int L, const LinearArgs& a, cudaStream_t st);
 cudaError_t launch_act_pack(int L, const PackArgs& a, cudaStream_t st);
 cudaError_t launch_attention(const AttnArgs& a, int n_blk, cudaStream_t st);
 size_t attention_smem_bytes(int qmax, int hpk, int hd, int ctx_cap);
+int attention_chunks(int ctx_cap);
+int attention_chunk_len();
 
 cudaError_t launch_quantize_weight(const QuantWArgs& a, cudaStream_t st);
 cudaError_t launch_lcg_fill(float* out, unsigned long long seed, unsigned long long offset, long long count,
@@ -41,6 +43,27 @@ int num_sms() {
     if (g_num_sms <= 0) g_num_sms = 148;
   }
   return g_num_sms;
+}
+
+// Optional per-linear event ring: when enabled, every linear launch issued by
+// qs_forward is bracketed by two events (captured as event nodes inside a CUDA
+// graph), so bench.py can attribute device time to the dominant kernel.
+struct Prof {
+  bool on = false;
+  int cap = 0, n = 0;
+  cudaEvent_t* ev = nullptr;
+  int32_t* tag = nullptr;
+} g_prof;
+
+void prof_mark(cudaStream_t st, int32_t tag, bool begin) {
+  if (!g_prof.on) return;
+  const int i = g_prof.n;
+  if (i >= g_prof.cap) return;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(st, &cs);
+  cudaEventRecordWithFlags(g_prof.ev[i], st, cs == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : 0);
+  if (begin) g_prof.tag[i / 2] = tag;
+  g_prof.n = i + 1;
 }
 
 int status(cudaError_t e) {
@@ -94,7 +117,7 @@ LinearArgs linear_args(const qs_qweight_t& w, int T, int L, const qs_workspace_t
   a.T = T;
   a.r_pad = img_rows(T, L);
   a.a_ld = round_up(T, 8);
-  const int U = w.n_tiles * w.G;
+  const int U = w.n_tiles * w.n_chunks;
   a.n_cta = U < num_sms() ? U : num_sms();
   a.part = ws->part;
   a.counters = ws->counters;
@@ -159,6 +182,36 @@ SeqState seq_state(const qs_seq_t* s) {
 
 extern "C" {
 
+int qs_profile_enable(int32_t max_launches) {
+  // events are never destroyed: graphs captured while profiling keep referencing them
+  g_prof.on = max_launches > 0;
+  if (!g_prof.on) return QS_OK;  // keep the recorded ring readable
+  g_prof.n = 0;
+  if (2 * max_launches <= g_prof.cap) return QS_OK;
+  g_prof.cap = 2 * max_launches;
+  g_prof.ev = new cudaEvent_t[g_prof.cap];
+  g_prof.tag = new int32_t[max_launches];
+  for (int i = 0; i < g_prof.cap; ++i)
+    if (cudaEventCreate(&g_prof.ev[i]) != cudaSuccess) return QS_ERR_CUDA;
+  return QS_OK;
+}
+
+int qs_profile_reset(void) {
+  g_prof.n = 0;
+  return QS_OK;
+}
+
+int qs_profile_read(float* ms, int32_t* tags, int32_t max_out, int32_t* n_out) {
+  const int n = g_prof.n / 2 < max_out ? g_prof.n / 2 : max_out;
+  for (int i = 0; i < n; ++i) {
+    if (cudaEventSynchronize(g_prof.ev[2 * i + 1]) != cudaSuccess) return QS_ERR_CUDA;
+    if (cudaEventElapsedTime(&ms[i], g_prof.ev[2 * i], g_prof.ev[2 * i + 1]) != cudaSuccess) return QS_ERR_CUDA;
+    tags[i] = g_prof.tag[i];
+  }
+  *n_out = n;
+  return QS_OK;
+}
+
 const char* qs_version(void) { return "qspec_b200 0.1 (sm_100a tcgen05 kind::i8)"; }
 
 int qs_num_sms(int32_t* out) {
@@ -195,11 +248,14 @@ int qs_workspace_size(const qs_model_t* m, int32_t t_max, qs_workspace_sizes_t* 
   out->attn = (size_t)t_max * m->d_model * 4;
   out->q = (size_t)t_max * m->n_heads * hd * 4;
   out->img = (size_t)chunks * img_rows(kMaxT, 3) * 128;
-  out->ascale = (size_t)groups * kMaxT * 4;
+  out->ascale = (size_t)chunks * kMaxT * 4;
   out->part = (size_t)(num_sms() + tiles) * kMaxT * kTileN * 4;
   out->counters = (size_t)(tiles + 1) * 4;
   out->arg_val = (size_t)wl.n_tiles * kMaxT * 4;
   out->arg_idx = (size_t)wl.n_tiles * kMaxT * 4;
+  const int cmax = attention_chunks(m->rope_len > 0 ? m->rope_len : 4096);
+  out->att_o = (size_t)t_max * m->n_heads * cmax * hd * 4;
+  out->att_ml = (size_t)t_max * m->n_heads * cmax * 8;
   return QS_OK;
 }
 
@@ -297,6 +353,23 @@ int qs_w4a16_linear(const qs_qweight_t* w, const float* x, int32_t T, float* y, 
   return run_linear(w, x, T, y, ws, 3, kOpStore, nullptr, (cudaStream_t)stream);
 }
 
+static unsigned long long* g_dbg = nullptr;
+int qs_debug_timeline(uint64_t* buf) {
+  g_dbg = reinterpret_cast<unsigned long long*>(buf);
+  return QS_OK;
+}
+
+int qs_linear_prepacked(const qs_qweight_t* w, int32_t T, int32_t mode, float* y, const qs_workspace_t* ws,
+                        void* stream) {
+  int rc = check_weight(w);
+  if (rc) return rc;
+  if (T < 1 || T > kMaxT || !ws) return QS_ERR_SHAPE;
+  const int L = mode == QS_MODE_LOW ? 1 : 3;
+  LinearArgs a = linear_args(*w, T, L, ws, kOpStore, y, w->n);
+  a.dbg = g_dbg;
+  return status(launch_linear(L, a, (cudaStream_t)stream));
+}
+
 int qs_linear_group_dots(const qs_qweight_t* w, const float* x, int32_t T, int32_t mode, int32_t* dots,
                          const qs_workspace_t* ws, void* stream) {
   return run_linear(w, x, T, nullptr, ws, mode == QS_MODE_LOW ? 1 : 3, kOpDump, dots, (cudaStream_t)stream);
@@ -310,7 +383,9 @@ int qs_forward(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const qs_
   const int L = mode == QS_MODE_LOW ? 1 : 3;
   const int d = m->d_model, H = m->n_heads, KV = m->n_kv_heads, hd = d / H, ff = m->d_ff;
   const int hpk = H / KV;
-  if (b->blk_qmax * hpk > 64 || b->blk_qmax * hpk * hd > 8192) return QS_ERR_SHAPE;
+  if (b->blk_qmax * hpk > 64 || hd % 4 != 0) return QS_ERR_SHAPE;
+  if (b->ctx_cap > m->rope_len) return QS_ERR_OVERFLOW;
+  const int att_cmax = attention_chunks(m->rope_len);
   if (attention_smem_bytes(b->blk_qmax, hpk, hd, b->ctx_cap) > 200 * 1024) return QS_ERR_SHAPE;
   cudaError_t e;
   for (int li = 0; li < m->n_layers; ++li) {
@@ -340,7 +415,9 @@ int qs_forward(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const qs_
     a.block_table = m->block_table;
     a.bt_ld = m->bt_ld;
     a.page = m->page;
+    prof_mark(st, mode * 16 + 0, true);
     if ((e = launch_linear(L, a, st)) != cudaSuccess) return status(e);
+    prof_mark(st, 0, false);
     // attention (model.py:293-330)
     AttnArgs at{};
     at.q = ws->q;
@@ -363,24 +440,39 @@ int qs_forward(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const qs_
     at.ctx_cap = b->ctx_cap;
     at.out = ws->attn;
     at.ldo = d;
+    at.part_o = ws->att_o;
+    at.part_ml = ws->att_ml;
+    at.cmax = att_cmax;
     if ((e = launch_attention(at, b->n_blk, st)) != cudaSuccess) return status(e);
-    // o_proj + residual (model.py:332)
+    // o_proj + residual (model.py:332); its operand pack merges the attention chunks
     p = pack_args(ly.o, ws->attn, d, T, ws, L);
+    p.att_o = ws->att_o;
+    p.att_ml = ws->att_ml;
+    p.att_pos = b->positions;
+    p.att_hd = hd;
+    p.att_cmax = att_cmax;
+    p.att_chunk = attention_chunk_len();
     if ((e = launch_act_pack(L, p, st)) != cudaSuccess) return status(e);
     a = linear_args(ly.o, T, L, ws, kOpResidual, ws->x, d);
+    prof_mark(st, mode * 16 + 1, true);
     if ((e = launch_linear(L, a, st)) != cudaSuccess) return status(e);
+    prof_mark(st, 0, false);
     // ffn rmsnorm -> gate|up with fused silu * up (model.py:333-335)
     p = pack_args(ly.gate_up, ws->x, d, T, ws, L);
     p.rms_w = ly.ffn_norm;
     p.eps = m->norm_eps;
     if ((e = launch_act_pack(L, p, st)) != cudaSuccess) return status(e);
     a = linear_args(ly.gate_up, T, L, ws, kOpSiluMul, ws->h, ff);
+    prof_mark(st, mode * 16 + 2, true);
     if ((e = launch_linear(L, a, st)) != cudaSuccess) return status(e);
+    prof_mark(st, 0, false);
     // down_proj + residual (model.py:336)
     p = pack_args(ly.down, ws->h, ff, T, ws, L);
     if ((e = launch_act_pack(L, p, st)) != cudaSuccess) return status(e);
     a = linear_args(ly.down, T, L, ws, kOpResidual, ws->x, d);
+    prof_mark(st, mode * 16 + 3, true);
     if ((e = launch_linear(L, a, st)) != cudaSuccess) return status(e);
+    prof_mark(st, 0, false);
   }
   // final norm + lm_head + argmax (model.py:342-344, numerics.py:81-86)
   PackArgs p = pack_args(m->lm_head, ws->x, d, T, ws, L);
@@ -389,7 +481,10 @@ int qs_forward(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const qs_
   if ((e = launch_act_pack(L, p, st)) != cudaSuccess) return status(e);
   LinearArgs a = linear_args(m->lm_head, T, L, ws, kOpLogits, logits, m->vocab);
   a.argmax_out = argmax;
-  return status(launch_linear(L, a, st));
+  prof_mark(st, mode * 16 + 4, true);
+  e = launch_linear(L, a, st);
+  prof_mark(st, 0, false);
+  return status(e);
 }
 
 int qs_draft_prep(const qs_seq_t* s, int32_t step, void* stream) {

@@ -61,10 +61,12 @@ __global__ void quantize_weight_kernel(const QuantWArgs a) {
   }
   const float s = __fdiv_rn(m, 7.0f);
   const int dst_row = a.row_off + n * a.row_stride;
-  a.scales[(size_t)gi * a.n_pad + dst_row] = s;
+  const int tile = dst_row / kTileN, r = dst_row % kTileN;
+  const int cpg = a.gp / kChunkK;
+  for (int cc = 0; cc < cpg; ++cc)  // scales per 128-wide chunk, tile-major [n_tiles][n_chunks][128]
+    a.scales[((size_t)tile * a.n_chunks + gi * cpg + cc) * kTileN + r] = s;
   if (a.ref_scales) a.ref_scales[(size_t)n * a.G + gi] = s;
   // pass 2: codes -> chunk layout.  Padded positions (o >= g) stay zero (buffer pre-zeroed).
-  const int tile = dst_row / kTileN, r = dst_row % kTileN;
   unsigned long long st = st0;
   uint8_t prev_ref = 0;
   for (int o = 0; o < g; ++o) {
@@ -118,8 +120,10 @@ __global__ void repack_ref_kernel(const uint8_t* ref_codes, const float* ref_sca
   if (idx >= (long long)rows * G) return;
   const int n = (int)(idx / G), gi = (int)(idx % G);
   const int dst_row = row_off + n * row_stride;
-  scales[(size_t)gi * n_pad + dst_row] = ref_scales[(size_t)n * G + gi];
   const int tile = dst_row / kTileN, r = dst_row % kTileN;
+  const int cpg = gp / kChunkK;
+  for (int cc = 0; cc < cpg; ++cc)
+    scales[((size_t)tile * n_chunks + gi * cpg + cc) * kTileN + r] = ref_scales[(size_t)n * G + gi];
   for (int o = 0; o < g; ++o) {
     const long long fe = (long long)n * cols + (long long)gi * g + o;
     const uint8_t byte = ref_codes[fe >> 1];

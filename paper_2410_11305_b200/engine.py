@@ -158,21 +158,48 @@ class DecodeEngine:
             self.graph = g
         self.graph.replay()
 
+    def profile_step(self) -> list[tuple[float, int]]:
+        """Replay one real step from a graph whose linear launches are bracketed by events.
+
+        Returns [(ms, tag)] per linear launch (tag = mode*16 + kind, see qspec_b200.h).
+        """
+        import torch
+        import ctypes as C
+        body = self._cycle_body if self.algorithm == "qspec" else self._ar_body
+        if self.graph is None:
+            self.step()           # ensures warm-up happened (attributes set)
+        n_max = 8192
+        _lib.call("qs_profile_enable", n_max)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            body()
+        _lib.call("qs_profile_enable", 0)
+        g.replay()
+        torch.cuda.synchronize()
+        ms = (C.c_float * n_max)()
+        tags = (C.c_int32 * n_max)()
+        n = _lib.i32()
+        _lib.call("qs_profile_read", C.addressof(ms), C.addressof(tags), n_max, C.byref(n))
+        self._prof_graph = g  # keep alive with its events
+        return [(float(ms[i]), int(tags[i])) for i in range(n.value)]
+
     # ------------------------------------------------------------------ admission
     def prefill(self, slot: int, prompt: list[int], max_new_tokens: int) -> None:
         """specdec.py:234-254: prompt through the HIGH path (greedy_mode for greedy), emit token 1."""
         import torch
         cfg = self.cfg
-        if not prompt:
+        if len(prompt) == 0:
             raise ShapeError("prompt must be non-empty")
         if len(prompt) + max_new_tokens > cfg.max_seq_len:
             raise SequenceOverflowError("prompt + max_new_tokens exceeds max_seq_len")
         if max_new_tokens > self.cap:
             raise ConfigError(f"max_new_tokens {max_new_tokens} exceeds engine capacity {self.cap}")
-        if min(prompt) < 0 or max(prompt) >= cfg.vocab_size:
-            raise TokenIdError("prompt token out of vocab range")
+        if not torch.is_tensor(prompt):
+            if min(prompt) < 0 or max(prompt) >= cfg.vocab_size:
+                raise TokenIdError("prompt token out of vocab range")
+            prompt = [int(t) for t in prompt]
         low = self.algorithm == "greedy" and self.greedy_low
-        _, argmax = run_forward_chunks(self.model, self.kv, [int(t) for t in prompt], 0, low, slot=slot)
+        _, argmax = run_forward_chunks(self.model, self.kv, prompt, 0, low, slot=slot)
         first = argmax[len(prompt) - 1:len(prompt)]
         b = slot
         self.t["pending"][b:b + 1].copy_(first)

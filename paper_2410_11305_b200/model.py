@@ -184,7 +184,7 @@ class TransformerModel:
             probe = _lib.Model(n_layers=self.config.n_layers, d_model=self.config.d_model,
                                n_heads=self.config.n_heads, n_kv_heads=self.config.n_kv_heads,
                                d_ff=self.config.d_ff, vocab=self.config.vocab_size,
-                               group_size=self.config.group_size)
+                               group_size=self.config.group_size, rope_len=self.rope_len)
             sizes = _lib.WorkspaceSizes()
             _lib.call("qs_workspace_size", probe, t_max, sizes)
             bufs = {n: torch.zeros(max(16, getattr(sizes, n)), dtype=torch.uint8, device="cuda")
@@ -346,14 +346,14 @@ def run_forward_chunks(model: TransformerModel, kv: KVCache, ids: list[int], bas
     logits = torch.empty((n, cfg.vocab_size), dtype=torch.float32, device="cuda")
     argmax = torch.empty(n, dtype=torch.int32, device="cuda")
     mode = _lib.QS_MODE_LOW if low else _lib.QS_MODE_HIGH
+    dev_ids = ids if torch.is_tensor(ids) else torch.tensor(ids, dtype=torch.int32).cuda()
+    dev_ids = dev_ids.to(device="cuda", dtype=torch.int32)
     for s in range(0, n, tmax):
-        chunk = ids[s:s + tmax]
-        T = len(chunk)
-        host = torch.tensor([chunk, list(range(base + s, base + s + T)), [slot] * T], dtype=torch.int32)
-        _bb.ids[:T].copy_(host[0], non_blocking=False)
-        _bb.pos[:T].copy_(host[1])
-        _bb.slot[:T].copy_(host[2])
-        _bb.blk.copy_(torch.tensor([0, T], dtype=torch.int32))
+        T = min(tmax, n - s)
+        _bb.ids[:T].copy_(dev_ids[s:s + T])
+        torch.arange(base + s, base + s + T, dtype=torch.int32, out=_bb.pos[:T])
+        _bb.slot[:T].fill_(slot)
+        _bb.blk[0], _bb.blk[1] = 0, T
         b = _lib.Batch(T=T, tokens=_bb.ids.data_ptr(), positions=_bb.pos.data_ptr(), slots=_bb.slot.data_ptr(),
                        n_blk=1, blk_tok0=_bb.blk.data_ptr(), blk_ntok=_bb.blk[1:].data_ptr(), blk_qmax=T,
                        ctx_cap=base + s + T)

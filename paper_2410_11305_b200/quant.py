@@ -93,13 +93,13 @@ def unpack_int4(packed: np.ndarray, count: int) -> np.ndarray:
 # ---------------------------------------------------------------- device store
 @dataclass
 class DeviceStore:
-    """Packed codes [n_tiles][n_chunks][4][128][16] + scales [G][n_pad] on the device."""
+    """Packed codes [n_tiles][n_chunks][4][128][16] + scales [n_tiles][n_chunks][128] on the device."""
 
     n: int
     k: int
     g: int
     codes: "object"   # torch.uint8 tensor
-    scales: "object"  # torch.float32 tensor [G, n_pad]
+    scales: "object"  # torch.float32 tensor [n_tiles, n_chunks, 128] (per 128-wide chunk, tile-major)
     geo: _lib.QWeight = field(repr=False)
 
     @classmethod
@@ -111,7 +111,7 @@ class DeviceStore:
         geo = _lib.QWeight()
         _lib.call("qs_qweight_geometry", n, k, g, geo)
         codes = torch.zeros(geo.n_tiles * geo.n_chunks * 8192, dtype=torch.uint8, device="cuda")
-        scales = torch.zeros((geo.G, geo.n_pad), dtype=torch.float32, device="cuda")
+        scales = torch.zeros((geo.n_tiles, geo.n_chunks, 128), dtype=torch.float32, device="cuda")
         geo.codes, geo.scales = codes.data_ptr(), scales.data_ptr()
         return cls(n, k, g, codes, scales, geo)
 
@@ -163,7 +163,10 @@ class QuantizedTensor:
 
     @property
     def scales(self) -> np.ndarray:
-        return self.store.scales.cpu().numpy().T[self._rows()].copy()
+        geo = self.store.geo
+        per_chunk = self.store.scales.cpu().numpy()[:, ::geo.cpg, :]          # [n_tiles, G, 128]
+        per_row = per_chunk.transpose(0, 2, 1).reshape(geo.n_pad, geo.G)
+        return per_row[self._rows()].copy()
 
     @property
     def is_view(self) -> bool:
@@ -238,9 +241,9 @@ class _LinearWorkspace:
             chunks = (k // g) * gp // 128
             sms = _lib.i32()
             _lib.call("qs_num_sms", C_byref(sms))
-            sizes = dict(x=4, h=4, attn=4, q=4, img=chunks * 192 * 128, ascale=(k // g) * 64 * 4,
+            sizes = dict(x=4, h=4, attn=4, q=4, img=chunks * 192 * 128, ascale=chunks * 64 * 4,
                          part=(sms.value + n_pad // 128) * 64 * 128 * 4, counters=(n_pad // 128 + 1) * 4,
-                         arg_val=(n_pad // 128) * 64 * 4, arg_idx=(n_pad // 128) * 64 * 4)
+                         arg_val=(n_pad // 128) * 64 * 4, arg_idx=(n_pad // 128) * 64 * 4, att_o=4, att_ml=4)
             self.bufs = {kk: torch.zeros(v, dtype=torch.uint8, device="cuda") for kk, v in sizes.items()}
             self.ws = _lib.Workspace(**{kk: b.data_ptr() for kk, b in self.bufs.items()})
             self.key = key
@@ -289,7 +292,7 @@ def linear_group_dots(q: QuantizedTensor, x, mode: ExecutionMode):
     L = 1 if mode is ExecutionMode.LOW_PRECISION else 3
     r = T * L
     r_pad = 8 if r <= 8 else -(-r // 16) * 16
-    dots = torch.zeros((st.geo.n_pad, st.geo.G, r_pad), dtype=torch.int32, device="cuda")
+    dots = torch.zeros((st.geo.n_pad, st.geo.n_chunks, r_pad), dtype=torch.int32, device="cuda")
     ws = _ws.get(st.n, st.k, st.g)
     _lib.call("qs_linear_group_dots", st.geo, t.data_ptr(), T,
               _lib.QS_MODE_LOW if L == 1 else _lib.QS_MODE_HIGH, dots.data_ptr(), ws, _lib.stream_ptr())
