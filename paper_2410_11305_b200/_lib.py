@@ -13,7 +13,7 @@ import os
 from .errors import ConfigError, QSpecError, SequenceOverflowError, ShapeError, TokenIdError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libqspec_b200.so")
+LIB_PATH = os.environ.get("QSPEC_LIB") or os.path.join(HERE, "libqspec_b200.so")
 
 QS_OK, QS_ERR_SHAPE, QS_ERR_CONFIG, QS_ERR_OVERFLOW, QS_ERR_TOKEN, QS_ERR_CUDA = range(6)
 QS_MODE_HIGH, QS_MODE_LOW = 0, 1

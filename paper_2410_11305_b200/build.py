@@ -43,7 +43,8 @@ def build(verbose: bool = False, force: bool = False) -> str:
         obj = os.path.join(BUILD, os.path.basename(src)[:-3] + ".o")
         objs.append(obj)
         if force or _stale(obj, [src] + headers):
-            jobs.append([NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj])
+            extra = []
+            jobs.append([NVCC, *ARCH, *FLAGS, *extra, "-c", src, "-o", obj])
 
     def run(cmd: list[str]) -> None:
         if verbose:

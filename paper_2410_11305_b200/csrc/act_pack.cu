@@ -12,169 +12,31 @@
 // Grid: (token, block of kGroupsPerCta groups), 32 threads per group.  A CTA
 // that needs RMSNorm re-reads the whole row for the sum of squares (L2-resident,
 // fixed reduction order, so every CTA of a token computes the same scale).
-#include "ptx.cuh"
-#include "qs_common.cuh"
+#include "pack_dev.cuh"
 
 namespace qs {
 
 constexpr int kGroupsPerCta = 4;
 constexpr int kPackThreads = 32 * kGroupsPerCta;
 
-__device__ __forceinline__ float snap_group_max(float m) {
-  // quant.py:163-176 (fixed point of m -> f32(7*f32(m/7)), <= 8 passes)
-  for (int it = 0; it < 8; ++it) {
-    const float nx = __fmul_rn(7.0f, __fdiv_rn(m, 7.0f));
-    if (nx == m) break;
-    m = nx;
-  }
-  return m;
-}
-
-// element k of the token's input row (gather / plain / attention combine)
-__device__ __forceinline__ float pack_load(const PackArgs& a, int t, int k, const float* src_row) {
-  if (a.att_o == nullptr) return src_row[k];
-  const int H = a.K / a.att_hd;
-  const int h = k / a.att_hd, d = k - h * a.att_hd;
-  const int nch = (a.att_pos[t] + a.att_chunk) / a.att_chunk;  // ceil((pos+1)/chunk)
-  const float2* ml = reinterpret_cast<const float2*>(a.att_ml) + ((size_t)t * H + h) * a.att_cmax;
-  const float* o = a.att_o + (((size_t)t * H + h) * a.att_cmax) * a.att_hd + d;
-  float M = -INFINITY;
-  for (int c = 0; c < nch; ++c) M = fmaxf(M, ml[c].x);
-  float Ls = 0.f, acc = 0.f;
-  for (int c = 0; c < nch; ++c) {
-    const float w = expf(ml[c].x - M);
-    Ls = fmaf(w, ml[c].y, Ls);
-    acc = fmaf(w, o[(size_t)c * a.att_hd], acc);
-  }
-  return __fdiv_rn(acc, Ls);
-}
-
 template <int L>
 __global__ void __launch_bounds__(kPackThreads) act_pack_kernel(const PackArgs a) {
   __shared__ float red[kGroupsPerCta];
+  pdl_launch_dependents();
+  pdl_wait();
   const int t = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int K = a.K;
-  const float* src_row = a.gather_ids != nullptr ? a.emb + (size_t)a.gather_ids[t] * K : a.x + (size_t)t * a.ldx;
-
   float inv = 1.0f;
-  if (a.rms_w != nullptr) {
-    // numerics.py:60: mean(x*x) -- fixed per-thread stride + fixed tree => same in every CTA
-    float part = 0.f;
-    for (int k = tid; k < K; k += kPackThreads) {
-      const float v = src_row[k];
-      part = __fadd_rn(part, __fmul_rn(v, v));
-    }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) part = __fadd_rn(part, __shfl_xor_sync(0xffffffffu, part, off));
-    if (lane == 0) red[warp] = part;
-    __syncthreads();
-    float ss = 0.f;
-    for (int w = 0; w < kGroupsPerCta; ++w) ss = __fadd_rn(ss, red[w]);
-    const float ms = __fdiv_rn(ss, (float)K);
-    inv = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(ms, a.eps)));
-  }
-
+  if (a.rms_w != nullptr) inv = token_inv_rms(a, t, tid, kPackThreads, 1, red);
   const int gi = blockIdx.y * kGroupsPerCta + warp;
   if (gi >= a.G) return;
-  const int g = a.g, cpg = a.gp >> 7;
-  // this lane's (up to 4 x 4) elements of the group, kept in registers
-  constexpr int kMaxIter = 4;  // gp <= 512
-  float val[kMaxIter][4];
-  float m = 0.f;
-#pragma unroll
-  for (int it = 0; it < kMaxIter; ++it) {
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int o = it * 128 + lane * 4 + e;
-      float v = 0.f;
-      if (o < g) {
-        const int k = gi * g + o;
-        v = pack_load(a, t, k, src_row);
-        if (a.x_out) a.x_out[(size_t)t * K + k] = v;
-        if (a.rms_w != nullptr) v = __fmul_rn(__fmul_rn(v, inv), a.rms_w[k]);
-        if (a.y_out) a.y_out[(size_t)t * K + k] = v;
-      }
-      val[it][e] = v;
-      m = fmaxf(m, fabsf(v));
-    }
-  }
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
-  float s, mul;
-  int e2 = 0;
-  if constexpr (L == 1) {
-    m = snap_group_max(m);
-    s = __fdiv_rn(m, 7.0f);
-    mul = s;
-  } else {
-    if (m > 0.f) {
-      int E;
-      frexpf(m, &E);
-      e2 = 22 - E;
-      mul = ldexpf(1.0f, -e2);
-    } else {
-      mul = 0.f;
-    }
-    s = mul;
-  }
-  if (lane == 0) {
-    if (a.ascale)  // per 128-wide chunk (a group spans gp/128 chunks)
-      for (int cc = 0; cc < cpg; ++cc) a.ascale[(size_t)(gi * cpg + cc) * a.a_ld + t] = mul;
-    if (a.scales_out) a.scales_out[(size_t)t * a.G + gi] = s;
-  }
-  const size_t chunk_stride = (size_t)a.r_pad * 128;
-#pragma unroll
-  for (int it = 0; it < kMaxIter; ++it) {
-    const int o = it * 128 + lane * 4;
-    if (it * 128 >= a.gp) break;
-    uint32_t w[L];
-#pragma unroll
-    for (int l = 0; l < L; ++l) w[l] = 0;
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      int code[L];
-#pragma unroll
-      for (int l = 0; l < L; ++l) code[l] = 0;
-      if (o + e < g) {
-        const float x = val[it][e];
-        if constexpr (L == 1) {
-          float qv = 0.f;
-          if (s != 0.f) qv = fminf(fmaxf(rintf(__fdiv_rn(x, s)), -8.0f), 7.0f);
-          code[0] = (int)qv;
-          const size_t kk = (size_t)gi * g + o + e;
-          if (a.codes_out) a.codes_out[(size_t)t * K + kk] = (int8_t)code[0];
-          if (a.fq_out) a.fq_out[(size_t)t * K + kk] = __fmul_rn((float)code[0], s);
-        } else {
-          const int X = (m > 0.f) ? __float2int_rn(ldexpf(x, e2)) : 0;
-          const int l0 = ((X + 128) & 255) - 128;
-          const int X1 = (X - l0) >> 8;
-          const int l1 = ((X1 + 128) & 255) - 128;
-          code[0] = l0;
-          code[1 % L] = l1;
-          code[2 % L] = (X1 - l1) >> 8;
-        }
-      }
-#pragma unroll
-      for (int l = 0; l < L; ++l) w[l] |= ((uint32_t)(code[l] & 0xFF)) << (8 * e);
-    }
-    if (a.img) {
-      const int kp = gi * a.gp + o;
-      const int ch = kp >> 7, byte = kp & 127;
-#pragma unroll
-      for (int l = 0; l < L; ++l)
-        *reinterpret_cast<uint32_t*>(a.img + ch * chunk_stride + sw128_off(t * L + l, byte)) = w[l];
-    }
-  }
+  pack_group<L>(a, t, gi, inv, lane);
 }
 
 cudaError_t launch_act_pack(int L, const PackArgs& a, cudaStream_t st) {
   if (a.gp > 512) return cudaErrorInvalidValue;
   const dim3 grid(a.T, (a.G + kGroupsPerCta - 1) / kGroupsPerCta);
-  if (L == 1)
-    act_pack_kernel<1><<<grid, kPackThreads, 0, st>>>(a);
-  else
-    act_pack_kernel<3><<<grid, kPackThreads, 0, st>>>(a);
-  return cudaGetLastError();
+  if (L == 1) return launch_k(act_pack_kernel<1>, grid, dim3(kPackThreads), 0, st, a);
+  return launch_k(act_pack_kernel<3>, grid, dim3(kPackThreads), 0, st, a);
 }
 
 }  // namespace qs

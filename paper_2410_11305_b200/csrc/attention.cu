@@ -26,6 +26,8 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 
 __global__ void __launch_bounds__(256) attn_partial_kernel(const AttnArgs a) {
   extern __shared__ __align__(16) float sm[];
+  pdl_launch_dependents();
+  pdl_wait();
   const int blk = blockIdx.x, kvh = blockIdx.y, ch = blockIdx.z, tid = threadIdx.x;
   const int ntok = a.blk_ntok[blk];
   if (ntok <= 0) return;
@@ -132,8 +134,7 @@ cudaError_t launch_attention(const AttnArgs& a, int n_blk, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     attr = smem;
   }
-  attn_partial_kernel<<<dim3(n_blk, a.KV, attention_chunks(a.ctx_cap)), 256, smem, st>>>(a);
-  return cudaGetLastError();
+  return launch_k(attn_partial_kernel, dim3(n_blk, a.KV, attention_chunks(a.ctx_cap)), dim3(256), smem, st, a);
 }
 
 }  // namespace qs

@@ -4,6 +4,7 @@
 // truncation and the reference's bookkeeping (specdec.py:258-317, 360-369,
 // 325-335).  Everything stays on the device so one CUDA graph replays a whole
 // draft-verify cycle for the batch with no host synchronisation.
+#include "ptx.cuh"
 #include "qs_common.cuh"
 
 namespace qs {
@@ -22,6 +23,8 @@ __device__ __forceinline__ void seq_finish_check(const SeqState& s, int b, int l
 
 // step j of the draft phase (specdec.py:103-133, 258-277)
 __global__ void draft_prep_kernel(const SeqState s, int j) {
+  pdl_launch_dependents();
+  pdl_wait();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= s.B) return;
   if (j == 0) {
@@ -41,6 +44,8 @@ __global__ void draft_prep_kernel(const SeqState s, int j) {
 
 // verify input [pending, drafted...] (specdec.py:136-156)
 __global__ void verify_prep_kernel(const SeqState s) {
+  pdl_launch_dependents();
+  pdl_wait();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= s.B) return;
   const int G1 = s.gamma + 1;
@@ -54,6 +59,8 @@ __global__ void verify_prep_kernel(const SeqState s) {
 
 // greedy acceptance + commit (specdec.py:159-176, 279-317)
 __global__ void accept_kernel(const SeqState s) {
+  pdl_launch_dependents();
+  pdl_wait();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= s.B || s.done[b]) return;
   const int G1 = s.gamma + 1;
@@ -101,6 +108,8 @@ __global__ void accept_kernel(const SeqState s) {
 
 // plain greedy decode step (specdec.py:325-335)
 __global__ void ar_prep_kernel(const SeqState s) {
+  pdl_launch_dependents();
+  pdl_wait();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= s.B) return;
   s.tok[b] = s.pending[b];
@@ -109,6 +118,8 @@ __global__ void ar_prep_kernel(const SeqState s) {
 }
 
 __global__ void ar_commit_kernel(const SeqState s) {
+  pdl_launch_dependents();
+  pdl_wait();
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= s.B || s.done[b]) return;
   const int nxt = s.argmax[b];
@@ -123,14 +134,13 @@ __global__ void ar_commit_kernel(const SeqState s) {
 cudaError_t launch_control(int op, const SeqState& s, int j, cudaStream_t st) {
   const int bs = 128, nb = (s.B + bs - 1) / bs;
   switch (op) {
-    case 0: draft_prep_kernel<<<nb, bs, 0, st>>>(s, j); break;
-    case 1: verify_prep_kernel<<<nb, bs, 0, st>>>(s); break;
-    case 2: accept_kernel<<<nb, bs, 0, st>>>(s); break;
-    case 3: ar_prep_kernel<<<nb, bs, 0, st>>>(s); break;
-    case 4: ar_commit_kernel<<<nb, bs, 0, st>>>(s); break;
+    case 0: return launch_k(draft_prep_kernel, dim3(nb), dim3(bs), 0, st, s, j);
+    case 1: return launch_k(verify_prep_kernel, dim3(nb), dim3(bs), 0, st, s);
+    case 2: return launch_k(accept_kernel, dim3(nb), dim3(bs), 0, st, s);
+    case 3: return launch_k(ar_prep_kernel, dim3(nb), dim3(bs), 0, st, s);
+    case 4: return launch_k(ar_commit_kernel, dim3(nb), dim3(bs), 0, st, s);
     default: return cudaErrorInvalidValue;
   }
-  return cudaGetLastError();
 }
 
 }  // namespace qs

@@ -28,21 +28,31 @@
 //               deterministic), fused post-op.
 // The reduction order of every output depends only on (N, K, grid), never on T,
 // so an n-token call is bit-identical to n single-token calls.
-#include "ptx.cuh"
-#include "qs_common.cuh"
+#include "pack_dev.cuh"
+
+// The fused operand-pack pre-phase (grid barrier inside the linear) is kept for
+// experiments; the default path packs in a separate PDL-overlapped launch.
+#ifndef QS_FUSED_PACK
+#define QS_FUSED_PACK 0
+#endif
 
 namespace qs {
 
 template <int L, int TMAX>
 struct LinCfg {
   static constexpr int kRowsMax = (L * TMAX) <= 8 ? 8 : ((L * TMAX + 15) / 16) * 16;
-  static constexpr int kAccCols = ((kRowsMax + 31) / 32) * 32;  // one accumulator block per chunk
-  // chunks per stage: as many as TMEM allows (2 acc buffers + 2 A slots)
+  static constexpr int kAccCols = kRowsMax;  // one accumulator block (N columns) per chunk
+  // chunks per stage: as many as TMEM allows with 2 acc buffers + 2 A slots
   static constexpr int kCPS = (2 * 4 * kAccCols + 2 * 4 * 32 <= 512) ? 4
                               : (2 * 2 * kAccCols + 2 * 2 * 32 <= 512) ? 2 : 1;
-  static constexpr int kAColBase = 2 * kCPS * kAccCols;
+  // spend leftover TMEM on deeper rings (lets unpack / epilogue run further ahead)
+  static constexpr int kFree0 = 512 - 2 * kCPS * kAccCols - 2 * kCPS * 32;
+  static constexpr int kASlots = 2 + (kFree0 >= kCPS * 32 ? 1 : 0);
+  static constexpr int kFree1 = kFree0 - (kASlots - 2) * kCPS * 32;
+  static constexpr int kAccBufs = 2 + (kFree1 / (kCPS * kAccCols) > 2 ? 2 : kFree1 / (kCPS * kAccCols));
+  static constexpr int kAColBase = kAccBufs * kCPS * kAccCols;
   static constexpr int kTmemCols = 512;
-  static_assert(kAColBase + 2 * kCPS * 32 <= kTmemCols, "TMEM budget");
+  static_assert(kAColBase + kASlots * kCPS * 32 <= kTmemCols, "TMEM budget");
   static constexpr int kActBytes = kRowsMax * 128;
   static constexpr int kStageBytes = kCPS * (kChunkBytes + kActBytes);
   static constexpr int kStages0 = (196 * 1024) / kStageBytes;
@@ -50,11 +60,19 @@ struct LinCfg {
   static_assert(kStages >= 2, "pipeline depth");
   static constexpr int kSStages = kStages + 2;
   static constexpr int kSEntry = kCPS * (128 + TMAX) * 4;
-  static constexpr int kOwnChunks = (TMAX / 8 + 1) / 2;  // token chunks per epilogue half
+  // 16 warps: 4 control, then unpack and epilogue warps (2 or 1 per TMEM lane
+  // quadrant each).  Small T is unpack-bound -> 8 unpack warps; large T is
+  // epilogue-bound -> 8 epilogue warps.
+  static constexpr int kUnpackWarps = TMAX <= 8 ? 8 : 4;
+  static constexpr int kEpiWarps = 12 - kUnpackWarps;
+  static constexpr int kEpiHalves = kEpiWarps / 4;
+  static constexpr int kUnpackHalves = kUnpackWarps / 4;
+  static constexpr int kEpiThreads = kEpiWarps * 32;
+  static constexpr int kOwnChunks = (TMAX / 8 + kEpiHalves - 1) / kEpiHalves;  // token chunks per epilogue warp
   static constexpr int kScaleOff = kStages * kStageBytes;
   static constexpr int kBarOff = kScaleOff + kSStages * kSEntry;
-  static constexpr int kNumBars = 2 * kStages + 4 + 4 + 2 * kSStages;
-  static constexpr int kSmemBytes = kBarOff + kNumBars * 8 + 16 + 4 * TMAX * 8 + 1024;
+  static constexpr int kNumBars = 3 * kStages + 2 * kASlots + 2 * kAccBufs + 2 * kSStages;
+  static constexpr int kSmemBytes = kBarOff + kNumBars * 8 + 16 + 4 * TMAX * 8 + 4 * 4 + 32 * 4 + 1024;
 };
 
 __device__ __forceinline__ uint32_t sext_nib(uint32_t n) {  // 4 nibbles (one per byte) -> 4 int8
@@ -102,19 +120,23 @@ __global__ void __launch_bounds__(512, 1) linear_tc_kernel(const LinearArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kBarOff);
-  uint64_t* full = bars;                       // [kStages] weights+act landed (tx bytes)
-  uint64_t* empty = full + C::kStages;         // [kStages] MMA commit -> producer
-  uint64_t* tfull = empty + C::kStages;        // [2] unpack -> MMA
-  uint64_t* tempty = tfull + 2;                // [2] MMA commit -> unpack
-  uint64_t* accfull = tempty + 2;              // [2] MMA commit -> epilogue
-  uint64_t* accempty = accfull + 2;            // [2] epilogue -> MMA
-  uint64_t* sfull = accempty + 2;              // [kSStages] scales landed
+  uint64_t* wfull = bars;                      // [kStages] stage weights landed (tx bytes)
+  uint64_t* afull = wfull + C::kStages;        // [kStages] stage activation image landed
+  uint64_t* empty = afull + C::kStages;        // [kStages] MMA commit -> producer
+  uint64_t* tfull = empty + C::kStages;        // [kASlots] unpack -> MMA
+  uint64_t* tempty = tfull + C::kASlots;       // [kASlots] MMA commit -> unpack
+  uint64_t* accfull = tempty + C::kASlots;     // [kAccBufs] MMA commit -> epilogue
+  uint64_t* accempty = accfull + C::kAccBufs;  // [kAccBufs] epilogue -> MMA
+  uint64_t* sfull = accempty + C::kAccBufs;    // [kSStages] scales landed
   uint64_t* sempty = sfull + C::kSStages;      // [kSStages] epilogue -> scale producer
   float* sring = reinterpret_cast<float*>(smem + C::kScaleOff);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::kNumBars);
   int* flag = reinterpret_cast<int*>(tmem_slot + 2);
   float* red_val = reinterpret_cast<float*>(tmem_slot + 4);  // [4][TMAX]
   int* red_idx = reinterpret_cast<int*>(red_val + 4 * TMAX);  // [4][TMAX]
+  volatile int* gen0_s = reinterpret_cast<volatile int*>(red_idx + 4 * TMAX);  // grid-barrier generation at entry
+  float* pk_red = reinterpret_cast<float*>(red_idx + 4 * TMAX + 4);            // [12] rms partials
+  float* pk_inv = pk_red + 16;                                                 // [4] per-token 1/rms
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int NC = a.n_chunks;
@@ -122,17 +144,25 @@ __global__ void __launch_bounds__(512, 1) linear_tc_kernel(const LinearArgs a) {
   const int u0 = unit_bound(c, U, P), u1 = unit_bound(c + 1, U, P);
   const bool dbg0 = a.dbg != nullptr && c == 0;
   if (a.dbg && threadIdx.x == 0) a.dbg[1024 + c] = gtimer();
+  pdl_launch_dependents();
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < C::kStages; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < C::kStages; ++i) {
+      mbar_init(&wfull[i], 1);
+      mbar_init(&afull[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < C::kASlots; ++i) {
       mbar_init(&tfull[i], 4);
       mbar_init(&tempty[i], 1);
-      mbar_init(&accfull[i], 1);
-      mbar_init(&accempty[i], 8);
     }
-    for (int i = 0; i < C::kSStages; ++i) { mbar_init(&sfull[i], 1); mbar_init(&sempty[i], 8); }
+    for (int i = 0; i < C::kAccBufs; ++i) {
+      mbar_init(&accfull[i], 1);
+      mbar_init(&accempty[i], C::kEpiWarps);
+    }
+    for (int i = 0; i < C::kSStages; ++i) { mbar_init(&sfull[i], 1); mbar_init(&sempty[i], C::kEpiWarps); }
     fence_mbar_init();
+    *gen0_s = -1;
   }
   if (warp == 2) tmem_alloc<C::kTmemCols>(tmem_slot);
   tc_fence_before();
@@ -141,23 +171,81 @@ __global__ void __launch_bounds__(512, 1) linear_tc_kernel(const LinearArgs a) {
   const uint32_t tmem = *tmem_slot;
   const uint32_t act_bytes = (uint32_t)a.r_pad * 128u;
 
+  // ---------------------------------------------------------------- fused pack pre-phase
+  // Warps 4..15 quantise this CTA's share of the (token, group) operand items into
+  // the global image while warp 0 is already streaming weights; a grid barrier
+  // (all CTAs are co-resident: grid <= #SMs, 1 CTA/SM) publishes the image before
+  // any activation copy is issued.
+#if QS_FUSED_PACK
+  if (a.fuse_pack && warp >= 4) {
+    pdl_wait();
+    const int ptid = threadIdx.x - 128;
+    if (ptid == 0) *gen0_s = ld_acquire(&a.gbar[1]);
+    const PackArgs& pk = a.pk;
+    const int TG = pk.T * pk.G;
+    const int p0 = (int)umul_div(c, TG, P), p1 = (int)umul_div(c + 1, TG, P);
+    if (p0 < p1) {
+      const int t_first = p0 / pk.G, t_last = (p1 - 1) / pk.G;
+      for (int tt = t_first; tt <= t_last; ++tt) {  // token by token: 1/rms, then its groups
+        float inv = 1.0f;
+        if (pk.rms_w != nullptr) {
+          inv = token_inv_rms(pk, tt, ptid, 384, 2, pk_red);
+        }
+        const int q0 = max(p0, tt * pk.G), q1 = min(p1, (tt + 1) * pk.G);
+        for (int p = q0 + (warp - 4); p < q1; p += 12) pack_group<L>(pk, tt, p - tt * pk.G, inv, lane);
+      }
+    }
+    fence_proxy_async_global();  // generic-proxy image writes -> later bulk (async-proxy) reads
+    named_bar(2, 384);
+    if (ptid == 0) {
+      const int old = atom_add_acq_rel(&a.gbar[0], 1);
+      if (old == P - 1) {
+        a.gbar[0] = 0;
+        red_release_add(&a.gbar[1], 1);
+      }
+    }
+  }
+#endif
+
   if (warp == 0) {
     // ------------------------------------------------------------ weight/act producer (warp-wide, elected issue)
+    // Weights do not depend on the previous kernel: the first kStages stages of
+    // weights are requested before griddepcontrol.wait (PDL overlap); activation
+    // images only after it.
     {
       StageIt it{u0, u1, NC, CPS};
-      for (int i = 0; it.next(); ++i) {
+      int npro = 0;
+      for (; npro < C::kStages && it.next(); ++npro) {
+        uint8_t* st = smem + npro * C::kStageBytes;
+        mbar_arrive_expect_tx_elect(&wfull[npro], (uint32_t)it.nq * kChunkBytes);
+        bulk_g2s_elect(st, a.codes + ((size_t)it.tile * NC + it.ch0) * kChunkBytes, it.nq * kChunkBytes,
+                       &wfull[npro]);
+      }
+      pdl_wait();
+      if (QS_FUSED_PACK && a.fuse_pack) grid_barrier_wait(gen0_s, a.gbar);
+      StageIt ia{u0, u1, NC, CPS};
+      for (int i = 0; i < npro && ia.next(); ++i) {
+        uint8_t* st = smem + i * C::kStageBytes;
+        mbar_arrive_expect_tx_elect(&afull[i], (uint32_t)ia.nq * act_bytes);
+        bulk_g2s_elect(st + CPS * kChunkBytes, a.act + (size_t)ia.ch0 * act_bytes, ia.nq * act_bytes, &afull[i]);
+        if (dbg0 && i < 64 && lane == 0) a.dbg[0 * 64 + i] = gtimer();
+      }
+      for (int i = npro; it.next(); ++i) {
         const int s = i % C::kStages;
         mbar_wait(&empty[s], ((i / C::kStages) & 1) ^ 1);
         uint8_t* st = smem + s * C::kStageBytes;
-        mbar_arrive_expect_tx_elect(&full[s], (uint32_t)it.nq * (kChunkBytes + act_bytes));
-        bulk_g2s_elect(st, a.codes + ((size_t)it.tile * NC + it.ch0) * kChunkBytes, it.nq * kChunkBytes, &full[s]);
-        bulk_g2s_elect(st + CPS * kChunkBytes, a.act + (size_t)it.ch0 * act_bytes, it.nq * act_bytes, &full[s]);
+        mbar_arrive_expect_tx_elect(&wfull[s], (uint32_t)it.nq * kChunkBytes);
+        bulk_g2s_elect(st, a.codes + ((size_t)it.tile * NC + it.ch0) * kChunkBytes, it.nq * kChunkBytes, &wfull[s]);
+        mbar_arrive_expect_tx_elect(&afull[s], (uint32_t)it.nq * act_bytes);
+        bulk_g2s_elect(st + CPS * kChunkBytes, a.act + (size_t)it.ch0 * act_bytes, it.nq * act_bytes, &afull[s]);
         if (dbg0 && i < 64 && lane == 0) a.dbg[0 * 64 + i] = gtimer();
       }
     }
   } else if (warp == 3) {
     // ------------------------------------------------------------ scale producer (warp-wide, elected issue)
     {
+      pdl_wait();
+      if (QS_FUSED_PACK && a.fuse_pack) grid_barrier_wait(gen0_s, a.gbar);
       const uint32_t a_bytes = (uint32_t)a.a_ld * 4u;
       StageIt it{u0, u1, NC, CPS};
       for (int i = 0; it.next(); ++i) {
@@ -175,40 +263,50 @@ __global__ void __launch_bounds__(512, 1) linear_tc_kernel(const LinearArgs a) {
       const uint32_t idesc = idesc_i8(128, (uint32_t)a.r_pad);
       StageIt it{u0, u1, NC, CPS};
       for (int i = 0; it.next(); ++i) {
-        const int s = i % C::kStages, b = i & 1;
+        const int s = i % C::kStages, b = i % C::kAccBufs, as_ = i % C::kASlots;
         if (dbg0 && i < 64 && lane == 0) a.dbg[4 * 64 + i] = gtimer();
-        mbar_wait(&accempty[b], ((i >> 1) & 1) ^ 1);
+        mbar_wait(&accempty[b], ((i / C::kAccBufs) & 1) ^ 1);
         if (dbg0 && i < 64 && lane == 0) a.dbg[5 * 64 + i] = gtimer();
-        mbar_wait(&full[s], (i / C::kStages) & 1);
+        mbar_wait(&afull[s], (i / C::kStages) & 1);
         if (dbg0 && i < 64 && lane == 0) a.dbg[6 * 64 + i] = gtimer();
-        mbar_wait(&tfull[b], (i >> 1) & 1);
+        mbar_wait(&tfull[as_], (i / C::kASlots) & 1);
         tc_fence_after();
         if (dbg0 && i < 64 && lane == 0) a.dbg[7 * 64 + i] = gtimer();
-        const uint32_t b_base = smem_u32(smem + s * C::kStageBytes + CPS * kChunkBytes);
-        for (int q = 0; q < it.nq; ++q) {
-          const uint32_t d_tmem = tmem + (b * CPS + q) * C::kAccCols;
-          const uint32_t a_tmem = tmem + C::kAColBase + (b * CPS + q) * 32;
-          const uint32_t bq = b_base + q * act_bytes;
+        // per-stage bases; every per-MMA offset below is a compile-time constant
+        // (the image chunk stride is kActBytes because r_pad == kRowsMax)
+        const uint64_t bdesc0 = sdesc_sw128(smem_u32(smem + s * C::kStageBytes + CPS * kChunkBytes));
+        const uint32_t d0 = tmem + b * CPS * C::kAccCols;
+        const uint32_t a0 = tmem + C::kAColBase + as_ * CPS * 32;
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk)
-            mma_i8_ts_elect(d_tmem, a_tmem + kk * 8, sdesc_sw128(bq + kk * 32), idesc, kk);
+        for (int q = 0; q < CPS; ++q) {
+          if (q < it.nq) {
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+              mma_i8_ts_elect(d0 + q * C::kAccCols, a0 + q * 32 + kk * 8,
+                              bdesc0 + (uint64_t)((q * C::kActBytes + kk * 32) >> 4), idesc, kk);
+          }
         }
         if (dbg0 && i < 64 && lane == 0) a.dbg[8 * 64 + i] = gtimer();
         mma_commit_elect(&empty[s]);
-        mma_commit_elect(&tempty[b]);
+        mma_commit_elect(&tempty[as_]);
         mma_commit_elect(&accfull[b]);
         if (dbg0 && i < 64 && lane == 0) a.dbg[2 * 64 + i] = gtimer();
       }
     }
-  } else if (warp >= 4 && warp < 8) {
+  } else if (warp >= 4 && warp < 4 + C::kUnpackWarps) {
     // ------------------------------------------------------------ unpack
-    const int q4 = warp & 3, r = q4 * 32 + lane;
+    // kUnpackHalves groups of 4 warps (one per TMEM lane quadrant); group ug
+    // unpacks the stages i with i % kUnpackHalves == ug, so consecutive stages'
+    // latency chains (LDS -> ALU -> tcgen05.st -> wait) overlap.
+    const int q4 = warp & 3, ug = (warp - 4) >> 2, r = q4 * 32 + lane;
     const uint32_t lane_base = (uint32_t)(q4 * 32) << 16;
     StageIt it{u0, u1, NC, CPS};
     for (int i = 0; it.next(); ++i) {
-      const int s = i % C::kStages, b = i & 1;
-      mbar_wait_warp(&full[s], (i / C::kStages) & 1, 20);
-      mbar_wait_warp(&tempty[b], ((i >> 1) & 1) ^ 1, 20);
+      if ((i % C::kUnpackHalves) != ug) continue;
+      const int s = i % C::kStages, b = i % C::kASlots;
+      mbar_wait_warp(&wfull[s], (i / C::kStages) & 1, 0);
+      if (a.dbg && i == 0 && r == 0) a.dbg[3072 + c] = gtimer();
+      mbar_wait_warp(&tempty[b], ((i / C::kASlots) & 1) ^ 1, 0);
       tc_fence_after();
       if (dbg0 && i < 64 && r == 0) a.dbg[9 * 64 + i] = gtimer();
       // all LDS of the stage first (latency overlap), then unpack + TMEM stores
@@ -231,11 +329,20 @@ __global__ void __launch_bounds__(512, 1) linear_tc_kernel(const LinearArgs a) {
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               const int m = jp * 4 + e;
+#if QS_EXP == 2
+              v[m] = ww[e];
+              v[16 + m] = ww[e];
+#else
               v[m] = sext_nib(ww[e] & 0x0F0F0F0Fu);
               v[16 + m] = sext_nib((ww[e] >> 4) & 0x0F0F0F0Fu);
+#endif
             }
           }
+#if QS_EXP == 1
+          if (v[0] == 0x12345678u && v[31] == 0x9abcdef0u) a.dbg[4000] = v[5] + v[17];
+#else
           tmem_st32(tmem + lane_base + C::kAColBase + (b * CPS + q) * 32, v);
+#endif
         }
       }
       tmem_wait_st();
@@ -244,22 +351,25 @@ __global__ void __launch_bounds__(512, 1) linear_tc_kernel(const LinearArgs a) {
       if (lane == 0) mbar_arrive(&tfull[b]);
       if (dbg0 && i < 64 && r == 0) a.dbg[1 * 64 + i] = gtimer();
     }
-  } else if (warp >= 8) {
+  } else if (warp >= 4 + C::kUnpackWarps) {
     // ------------------------------------------------------------ epilogue
     // lane quadrant q4 = warp & 3 (TMEM lanes 32q4.. = tile rows); half h owns the
     // token chunks tc with (tc & 1) == h.
-    const int q4 = warp & 3, h = (warp - 8) >> 2, r = q4 * 32 + lane, et = threadIdx.x - 256;
+    constexpr int kH = C::kEpiHalves, kEpiT = C::kEpiThreads;
+    const int q4 = warp & 3, h = (warp - 4 - C::kUnpackWarps) >> 2, r = q4 * 32 + lane;
+    const int et = threadIdx.x - 32 * (4 + C::kUnpackWarps);
     const uint32_t lane_base = (uint32_t)(q4 * 32) << 16;
     constexpr int kOwn = C::kOwnChunks;
+    pdl_wait();  // epilogue reads / writes predecessor-owned buffers
     float acc[kOwn * 8];
 #pragma unroll
     for (int t = 0; t < kOwn * 8; ++t) acc[t] = 0.f;
     StageIt it{u0, u1, NC, CPS};
     for (int i = 0; it.next(); ++i) {
-      const int b = i & 1, ss = i % C::kSStages;
+      const int b = i % C::kAccBufs, ss = i % C::kSStages;
       const int tile = it.tile, n = tile * kTileN + r;
-      mbar_wait_warp(&sfull[ss], (i / C::kSStages) & 1, 64);
-      mbar_wait_warp(&accfull[b], (i >> 1) & 1, 64);
+      mbar_wait_warp(&sfull[ss], (i / C::kSStages) & 1, 0);
+      mbar_wait_warp(&accfull[b], (i / C::kAccBufs) & 1, 0);
       tc_fence_after();
       if (dbg0 && i < 64 && et == 0) a.dbg[10 * 64 + i] = gtimer();
       const float* se = sring + ss * (C::kSEntry / 4);
@@ -282,7 +392,7 @@ __global__ void __launch_bounds__(512, 1) linear_tc_kernel(const LinearArgs a) {
         for (int q = 0; q < CPS; ++q) sw[q] = (q < it.nq) ? se[q * 128 + r] : 0.f;
 #pragma unroll
         for (int lc = 0; lc < kOwn; ++lc) {
-          const int tc = 2 * lc + h;
+          const int tc = kH * lc + h;
           if (tc * 8 < a.T) {
             // one TMEM round trip per token chunk for all chunks of the stage
             uint32_t rr[CPS][8 * L];
@@ -336,41 +446,55 @@ __global__ void __launch_bounds__(512, 1) linear_tc_kernel(const LinearArgs a) {
       const int last_u = tile * NC + it.ch0 + it.nq - 1;
       const bool seg_end = (it.ch0 + it.nq == NC) || (last_u == u1 - 1);
       if (!seg_end || a.op == kOpDump) continue;
+      if (a.dbg && et == 0) a.dbg[3584 + c] = gtimer();
       const int c_lo = cta_of_unit(tile * NC, U, P);
       const int c_hi = cta_of_unit(tile * NC + NC - 1, U, P);
       if (c_hi > c_lo) {
-        float* my = a.part + ((size_t)(c + tile) * TMAX) * kTileN;
-#pragma unroll
-        for (int lc = 0; lc < kOwn; ++lc)
-#pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const int t = (2 * lc + h) * 8 + e;
-            if (t < a.T) my[t * kTileN + r] = acc[lc * 8 + e];
-          }
-        __threadfence();
-        named_bar(1, 256);
-        if (et == 0) {
-          const int old = atomicAdd(&a.counters[tile], 1);
-          *flag = (old == c_hi - c_lo);
-        }
-        named_bar(1, 256);
-        const int last = *flag;
-        named_bar(1, 256);
-#pragma unroll
-        for (int t = 0; t < kOwn * 8; ++t) acc[t] = 0.f;
-        if (!last) continue;
-        __threadfence();
-        for (int cc2 = c_lo; cc2 <= c_hi; ++cc2) {
-          const volatile float* pp = a.part + ((size_t)(cc2 + tile) * TMAX) * kTileN;
+        // Tile split across CTAs c_lo..c_hi.  Non-owners publish their partial and
+        // leave (release-increment, no round trip); the owner c_lo -- whose segment
+        // of this tile is the last one it processes -- waits for the others and sums
+        // in CTA order (deterministic: acc(c_lo) + p(c_lo+1) + ... + p(c_hi)).
+        if (c != c_lo) {
+          float* my = a.part + ((size_t)(c + tile) * TMAX) * kTileN;
 #pragma unroll
           for (int lc = 0; lc < kOwn; ++lc)
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
-              const int t = (2 * lc + h) * 8 + e;
-              if (t < a.T) acc[lc * 8 + e] = __fadd_rn(acc[lc * 8 + e], pp[t * kTileN + r]);
+              const int t = (kH * lc + h) * 8 + e;
+              if (t < a.T) __stcg(my + t * kTileN + r, acc[lc * 8 + e]);
             }
+          named_bar(1, kEpiT);
+          if (et == 0) red_release_add(&a.counters[tile], 1);
+#pragma unroll
+          for (int t = 0; t < kOwn * 8; ++t) acc[t] = 0.f;
+          continue;
         }
-        if (et == 0) a.counters[tile] = 0;
+        if (et == 0) {
+          while (ld_acquire(&a.counters[tile]) != c_hi - c_lo) {
+          }
+          a.counters[tile] = 0;
+        }
+        named_bar(1, kEpiT);
+        constexpr int kPB = kOwn <= 1 ? 4 : (kOwn == 2 ? 2 : 1);
+        for (int cb = c_lo + 1; cb <= c_hi; cb += kPB) {
+          float pv[kPB][kOwn * 8];
+#pragma unroll
+          for (int u = 0; u < kPB; ++u) {
+            const float* pp = a.part + ((size_t)(cb + u + tile) * TMAX) * kTileN;
+#pragma unroll
+            for (int lc = 0; lc < kOwn; ++lc)
+#pragma unroll
+              for (int e = 0; e < 8; ++e) {
+                const int t = (kH * lc + h) * 8 + e;
+                pv[u][lc * 8 + e] = (cb + u <= c_hi && t < a.T) ? __ldcg(pp + t * kTileN + r) : 0.f;
+              }
+          }
+#pragma unroll
+          for (int u = 0; u < kPB; ++u)
+            if (cb + u <= c_hi)
+#pragma unroll
+              for (int k2 = 0; k2 < kOwn * 8; ++k2) acc[k2] = __fadd_rn(acc[k2], pv[u][k2]);
+        }
       }
       // ---------------------------------------------------------- post-ops
       const bool valid = n < a.n;
@@ -378,7 +502,7 @@ __global__ void __launch_bounds__(512, 1) linear_tc_kernel(const LinearArgs a) {
       for (int lc = 0; lc < kOwn; ++lc) {
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-          const int t = (2 * lc + h) * 8 + e;
+          const int t = (kH * lc + h) * 8 + e;
           const float v = acc[lc * 8 + e];
           if (a.op == kOpStore || a.op == kOpResidual) {
             if (t < a.T && valid) {
@@ -431,7 +555,7 @@ __global__ void __launch_bounds__(512, 1) linear_tc_kernel(const LinearArgs a) {
         }
       }
       if (a.op == kOpLogits) {
-        named_bar(1, 256);
+        named_bar(1, kEpiT);
         if (et < a.T) {
           float bv = red_val[et];
           int bi = red_idx[et];
@@ -444,14 +568,14 @@ __global__ void __launch_bounds__(512, 1) linear_tc_kernel(const LinearArgs a) {
           a.arg_idx[(size_t)tile * TMAX + et] = bi;
         }
         __threadfence();
-        named_bar(1, 256);
+        named_bar(1, kEpiT);
         if (et == 0) {
           const int old = atomicAdd(&a.counters[a.n_tiles], 1);
           *flag = (old == a.n_tiles - 1);
         }
-        named_bar(1, 256);
+        named_bar(1, kEpiT);
         const int last = *flag;
-        named_bar(1, 256);
+        named_bar(1, kEpiT);
         if (last) {
           __threadfence();
           if (et < a.T) {
@@ -485,6 +609,7 @@ __global__ void __launch_bounds__(512, 1) linear_tc_kernel(const LinearArgs a) {
 template <int L, int TMAX>
 static cudaError_t launch_linear_t(const LinearArgs& a, cudaStream_t st) {
   using C = LinCfg<L, TMAX>;
+  if (a.r_pad != C::kRowsMax) return cudaErrorInvalidValue;  // image rows are padded to the bucket
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(linear_tc_kernel<L, TMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -492,8 +617,7 @@ static cudaError_t launch_linear_t(const LinearArgs& a, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  linear_tc_kernel<L, TMAX><<<a.n_cta, 512, C::kSmemBytes, st>>>(a);
-  return cudaGetLastError();
+  return launch_k(linear_tc_kernel<L, TMAX>, dim3(a.n_cta), dim3(512), C::kSmemBytes, st, a);
 }
 
 int linear_tmax_bucket(int T) { return T <= 8 ? 8 : T <= 16 ? 16 : T <= 32 ? 32 : 64; }

@@ -52,7 +52,12 @@ __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
 // Keeps the SM's barrier unit free for the producer / MMA threads.
 __device__ __forceinline__ void mbar_wait_warp(uint64_t* bar, uint32_t parity, uint32_t backoff_ns = 32) {
   if ((threadIdx.x & 31) == 0) {
-    while (!mbar_try(bar, parity)) __nanosleep(backoff_ns);
+    if (backoff_ns == 0) {
+      while (!mbar_try(bar, parity)) {
+      }
+    } else {
+      while (!mbar_try(bar, parity)) __nanosleep(backoff_ns);
+    }
   }
   __syncwarp();
 }
@@ -211,6 +216,43 @@ __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t smem_addr) {
   d |= (uint64_t)1 << 46;                        // descriptor version (sm100)
   d |= (uint64_t)2 << 61;                        // SWIZZLE_128B
   return d;
+}
+
+// Programmatic dependent launch: let the next kernel in the stream start its
+// prologue now; block until every prerequisite grid has completed and its
+// memory is visible.
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+__device__ __forceinline__ void red_release_add(int* p, int v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ int atom_add_acq_rel(int* p, int v) {
+  int old;
+  asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+// Warp-wide wait for the kernel's grid barrier: generation must move past the
+// value sampled (into smem) by the pack threads before they arrived.
+__device__ __forceinline__ void grid_barrier_wait(volatile int* gen0_s, int* gbar) {
+  if ((threadIdx.x & 31) == 0) {
+    int g0;
+    while ((g0 = *gen0_s) < 0) {
+    }
+    while (ld_acquire(&gbar[1]) == g0) {
+    }
+    fence_proxy_async_global();
+  }
+  __syncwarp();
 }
 
 __device__ __forceinline__ unsigned long long gtimer() {

@@ -17,8 +17,29 @@
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <utility>
 
 namespace qs {
+
+// Launch with programmatic stream serialisation (PDL): the kernel may start while
+// its predecessor drains; every forward-path kernel calls pdl_wait() before it
+// touches predecessor outputs.  QS_NO_PDL=1 in the environment disables it.
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                            Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 constexpr int kTileN = 128;    // output rows per tile (UMMA M)
 constexpr int kChunkK = 128;   // K positions per chunk (one SW128 row of int8)
@@ -39,6 +60,28 @@ enum PostOp : int {
   kOpQkvRope = 3,   // rope(q) -> out, rope(k) -> K cache, v -> V cache
   kOpLogits = 4,    // logits (optional store) + fused argmax
   kOpDump = 5,      // debug: raw int32 group dots
+};
+
+struct PackArgs {
+  const float* x;
+  int ldx;
+  const int* gather_ids;
+  const float* emb;
+  float* x_out;
+  const float* rms_w;
+  float eps;
+  int T, K, g, gp, G, n_chunks, r_pad, a_ld;
+  uint8_t* img;
+  float* ascale;
+  int8_t* codes_out;
+  float* scales_out;
+  float* fq_out;
+  float* y_out;
+  // attention combine mode (o_proj operand): x[t, h*hd+d] = sum_c w_c o_c[d] / sum_c w_c l_c
+  const float* att_o;   // [T][H][cmax][hd]
+  const float* att_ml;  // [T][H][cmax][2]  (chunk max, chunk sum)
+  const int* att_pos;   // [T] query positions (context = pos + 1)
+  int att_hd, att_cmax, att_chunk;
 };
 
 struct LinearArgs {
@@ -70,32 +113,16 @@ struct LinearArgs {
   int* argmax_out;
   // kOpDump
   int32_t* dump;
+  // fused operand pack pre-phase (replaces a separate act_pack launch)
+  PackArgs pk;
+  int fuse_pack;
+  int* gbar;  // [2] grid barrier: arrival count, generation
   // debug timeline (CTA 0): [role][i] globaltimer ns; roles: 0 producer issue, 1 unpack done,
   // 2 mma issued, 3 epilogue start (acc ready), 4 epilogue done
   unsigned long long* dbg;
 };
 
-struct PackArgs {
-  const float* x;
-  int ldx;
-  const int* gather_ids;
-  const float* emb;
-  float* x_out;
-  const float* rms_w;
-  float eps;
-  int T, K, g, gp, G, n_chunks, r_pad, a_ld;
-  uint8_t* img;
-  float* ascale;
-  int8_t* codes_out;
-  float* scales_out;
-  float* fq_out;
-  float* y_out;
-  // attention combine mode (o_proj operand): x[t, h*hd+d] = sum_c w_c o_c[d] / sum_c w_c l_c
-  const float* att_o;   // [T][H][cmax][hd]
-  const float* att_ml;  // [T][H][cmax][2]  (chunk max, chunk sum)
-  const int* att_pos;   // [T] query positions (context = pos + 1)
-  int att_hd, att_cmax, att_chunk;
-};
+
 
 struct AttnArgs {
   const float* q;

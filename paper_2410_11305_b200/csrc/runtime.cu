@@ -5,12 +5,14 @@
 // draft/verify cycles into CUDA graphs.
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 
 #include "../../include/qspec_b200.h"
 #include "qs_common.cuh"
 
 namespace qs {
 cudaError_t launch_linear(int L, const LinearArgs& a, cudaStream_t st);
+int linear_tmax_bucket(int T);
 cudaError_t launch_act_pack(int L, const PackArgs& a, cudaStream_t st);
 cudaError_t launch_attention(const AttnArgs& a, int n_blk, cudaStream_t st);
 size_t attention_smem_bytes(int qmax, int hpk, int hd, int ctx_cap);
@@ -29,9 +31,28 @@ cudaError_t launch_control(int op, const SeqState& s, int j, cudaStream_t st);
 
 using namespace qs;
 
+namespace qs {
+bool fuse_pack_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    on = 0;  // fused pre-phase compiled out (QS_FUSED_PACK=0 in linear_tc.cu)
+  }
+  return on == 1;
+}
+bool pdl_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("QS_NO_PDL");
+    on = (e && e[0] == '1') ? 0 : 1;
+  }
+  return on == 1;
+}
+}  // namespace qs
+
 namespace {
 
 constexpr int kMaxT = 64;
+constexpr int kGbarOffset = 4096;  // grid-barrier words live past every per-tile counter
 
 int g_num_sms = 0;
 
@@ -66,6 +87,24 @@ void prof_mark(cudaStream_t st, int32_t tag, bool begin) {
   g_prof.n = i + 1;
 }
 
+}  // namespace
+namespace qs {
+bool fuse_pack_enabled();
+}
+namespace {
+
+// Launch a linear whose operand comes from a.pk: either fused into the linear's
+// pre-phase (grid barrier) or as a separate act_pack launch overlapped via PDL.
+cudaError_t launch_linear_packed(int L, LinearArgs& a, cudaStream_t st) {
+  if (fuse_pack_enabled()) {
+    return launch_linear(L, a, st);
+  }
+  a.fuse_pack = 0;
+  cudaError_t e = launch_act_pack(L, a.pk, st);
+  if (e != cudaSuccess) return e;
+  return launch_linear(L, a, st);
+}
+
 int status(cudaError_t e) {
   if (e == cudaSuccess) return QS_OK;
   fprintf(stderr, "[qspec_b200] CUDA error: %s\n", cudaGetErrorString(e));
@@ -94,7 +133,7 @@ PackArgs pack_args(const qs_qweight_t& w, const float* x, int ldx, int T, const 
   p.gp = w.gp;
   p.G = w.G;
   p.n_chunks = w.n_chunks;
-  p.r_pad = img_rows(T, L);
+  p.r_pad = img_rows(linear_tmax_bucket(T), L);
   p.a_ld = round_up(T, 8);
   p.img = ws->img;
   p.ascale = ws->ascale;
@@ -115,7 +154,7 @@ LinearArgs linear_args(const qs_qweight_t& w, int T, int L, const qs_workspace_t
   a.cpg = w.cpg;
   a.n_chunks = w.n_chunks;
   a.T = T;
-  a.r_pad = img_rows(T, L);
+  a.r_pad = img_rows(linear_tmax_bucket(T), L);
   a.a_ld = round_up(T, 8);
   const int U = w.n_tiles * w.n_chunks;
   a.n_cta = U < num_sms() ? U : num_sms();
@@ -126,6 +165,7 @@ LinearArgs linear_args(const qs_qweight_t& w, int T, int L, const qs_workspace_t
   a.ldo = ldo;
   a.arg_val = ws->arg_val;
   a.arg_idx = ws->arg_idx;
+  a.gbar = ws->counters + kGbarOffset;
   return a;
 }
 
@@ -140,12 +180,10 @@ int run_linear(const qs_qweight_t* w, const float* x, int T, float* y, const qs_
   int rc = check_weight(w);
   if (rc) return rc;
   if (T < 1 || T > kMaxT || !x || !ws) return QS_ERR_SHAPE;
-  PackArgs p = pack_args(*w, x, w->k, T, ws, L);
-  cudaError_t e = launch_act_pack(L, p, st);
-  if (e != cudaSuccess) return status(e);
   LinearArgs a = linear_args(*w, T, L, ws, op, y, w->n);
+  a.pk = pack_args(*w, x, w->k, T, ws, L);
   a.dump = dump;
-  return status(launch_linear(L, a, st));
+  return status(launch_linear_packed(L, a, st));
 }
 
 SeqState seq_state(const qs_seq_t* s) {
@@ -250,7 +288,8 @@ int qs_workspace_size(const qs_model_t* m, int32_t t_max, qs_workspace_sizes_t* 
   out->img = (size_t)chunks * img_rows(kMaxT, 3) * 128;
   out->ascale = (size_t)chunks * kMaxT * 4;
   out->part = (size_t)(num_sms() + tiles) * kMaxT * kTileN * 4;
-  out->counters = (size_t)(tiles + 1) * 4;
+  out->counters = (size_t)(kGbarOffset + 2) * 4;
+  if (tiles + 1 > kGbarOffset) return QS_ERR_SHAPE;
   out->arg_val = (size_t)wl.n_tiles * kMaxT * 4;
   out->arg_idx = (size_t)wl.n_tiles * kMaxT * 4;
   const int cmax = attention_chunks(m->rope_len > 0 ? m->rope_len : 4096);
@@ -390,18 +429,17 @@ int qs_forward(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const qs_
   cudaError_t e;
   for (int li = 0; li < m->n_layers; ++li) {
     const qs_layer_t& ly = m->layers[li];
-    // attn rmsnorm (+ embedding gather on layer 0) -> activation operand
-    PackArgs p = pack_args(ly.qkv, ws->x, d, T, ws, L);
-    p.rms_w = ly.attn_norm;
-    p.eps = m->norm_eps;
-    if (li == 0) {
-      p.gather_ids = b->tokens;
-      p.emb = m->tok_emb;
-      p.x_out = ws->x;
-    }
-    if ((e = launch_act_pack(L, p, st)) != cudaSuccess) return status(e);
-    // q|k|v projection, fused RoPE + KV write (model.py:305-309, 339-340)
+    // q|k|v projection; operand = rmsnorm(x) (+ embedding gather on layer 0), fused
+    // pre-phase; epilogue: RoPE + KV write (model.py:302-309, 339-340)
     LinearArgs a = linear_args(ly.qkv, T, L, ws, kOpQkvRope, ws->q, H * hd);
+    a.pk = pack_args(ly.qkv, ws->x, d, T, ws, L);
+    a.pk.rms_w = ly.attn_norm;
+    a.pk.eps = m->norm_eps;
+    if (li == 0) {
+      a.pk.gather_ids = b->tokens;
+      a.pk.emb = m->tok_emb;
+      a.pk.x_out = ws->x;
+    }
     a.pos = b->positions;
     a.slot = b->slots;
     a.rope_cos = m->rope_cos;
@@ -416,9 +454,9 @@ int qs_forward(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const qs_
     a.bt_ld = m->bt_ld;
     a.page = m->page;
     prof_mark(st, mode * 16 + 0, true);
-    if ((e = launch_linear(L, a, st)) != cudaSuccess) return status(e);
+    if ((e = launch_linear_packed(L, a, st)) != cudaSuccess) return status(e);
     prof_mark(st, 0, false);
-    // attention (model.py:293-330)
+    // attention (model.py:293-330), split-KV partials
     AttnArgs at{};
     at.q = ws->q;
     at.ldq = H * hd;
@@ -444,45 +482,41 @@ int qs_forward(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const qs_
     at.part_ml = ws->att_ml;
     at.cmax = att_cmax;
     if ((e = launch_attention(at, b->n_blk, st)) != cudaSuccess) return status(e);
-    // o_proj + residual (model.py:332); its operand pack merges the attention chunks
-    p = pack_args(ly.o, ws->attn, d, T, ws, L);
-    p.att_o = ws->att_o;
-    p.att_ml = ws->att_ml;
-    p.att_pos = b->positions;
-    p.att_hd = hd;
-    p.att_cmax = att_cmax;
-    p.att_chunk = attention_chunk_len();
-    if ((e = launch_act_pack(L, p, st)) != cudaSuccess) return status(e);
+    // o_proj + residual (model.py:332); its fused pre-phase merges the attention chunks
     a = linear_args(ly.o, T, L, ws, kOpResidual, ws->x, d);
+    a.pk = pack_args(ly.o, ws->attn, d, T, ws, L);
+    a.pk.att_o = ws->att_o;
+    a.pk.att_ml = ws->att_ml;
+    a.pk.att_pos = b->positions;
+    a.pk.att_hd = hd;
+    a.pk.att_cmax = att_cmax;
+    a.pk.att_chunk = attention_chunk_len();
     prof_mark(st, mode * 16 + 1, true);
-    if ((e = launch_linear(L, a, st)) != cudaSuccess) return status(e);
+    if ((e = launch_linear_packed(L, a, st)) != cudaSuccess) return status(e);
     prof_mark(st, 0, false);
-    // ffn rmsnorm -> gate|up with fused silu * up (model.py:333-335)
-    p = pack_args(ly.gate_up, ws->x, d, T, ws, L);
-    p.rms_w = ly.ffn_norm;
-    p.eps = m->norm_eps;
-    if ((e = launch_act_pack(L, p, st)) != cudaSuccess) return status(e);
+    // gate|up on rmsnorm(x), epilogue silu(gate) * up (model.py:333-335)
     a = linear_args(ly.gate_up, T, L, ws, kOpSiluMul, ws->h, ff);
+    a.pk = pack_args(ly.gate_up, ws->x, d, T, ws, L);
+    a.pk.rms_w = ly.ffn_norm;
+    a.pk.eps = m->norm_eps;
     prof_mark(st, mode * 16 + 2, true);
-    if ((e = launch_linear(L, a, st)) != cudaSuccess) return status(e);
+    if ((e = launch_linear_packed(L, a, st)) != cudaSuccess) return status(e);
     prof_mark(st, 0, false);
     // down_proj + residual (model.py:336)
-    p = pack_args(ly.down, ws->h, ff, T, ws, L);
-    if ((e = launch_act_pack(L, p, st)) != cudaSuccess) return status(e);
     a = linear_args(ly.down, T, L, ws, kOpResidual, ws->x, d);
+    a.pk = pack_args(ly.down, ws->h, ff, T, ws, L);
     prof_mark(st, mode * 16 + 3, true);
-    if ((e = launch_linear(L, a, st)) != cudaSuccess) return status(e);
+    if ((e = launch_linear_packed(L, a, st)) != cudaSuccess) return status(e);
     prof_mark(st, 0, false);
   }
   // final norm + lm_head + argmax (model.py:342-344, numerics.py:81-86)
-  PackArgs p = pack_args(m->lm_head, ws->x, d, T, ws, L);
-  p.rms_w = m->final_norm;
-  p.eps = m->norm_eps;
-  if ((e = launch_act_pack(L, p, st)) != cudaSuccess) return status(e);
   LinearArgs a = linear_args(m->lm_head, T, L, ws, kOpLogits, logits, m->vocab);
+  a.pk = pack_args(m->lm_head, ws->x, d, T, ws, L);
+  a.pk.rms_w = m->final_norm;
+  a.pk.eps = m->norm_eps;
   a.argmax_out = argmax;
   prof_mark(st, mode * 16 + 4, true);
-  e = launch_linear(L, a, st);
+  e = launch_linear_packed(L, a, st);
   prof_mark(st, 0, false);
   return status(e);
 }

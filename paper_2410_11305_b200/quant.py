@@ -242,7 +242,7 @@ class _LinearWorkspace:
             sms = _lib.i32()
             _lib.call("qs_num_sms", C_byref(sms))
             sizes = dict(x=4, h=4, attn=4, q=4, img=chunks * 192 * 128, ascale=chunks * 64 * 4,
-                         part=(sms.value + n_pad // 128) * 64 * 128 * 4, counters=(n_pad // 128 + 1) * 4,
+                         part=(sms.value + n_pad // 128) * 64 * 128 * 4, counters=(4096 + 2) * 4,
                          arg_val=(n_pad // 128) * 64 * 4, arg_idx=(n_pad // 128) * 64 * 4, att_o=4, att_ml=4)
             self.bufs = {kk: torch.zeros(v, dtype=torch.uint8, device="cuda") for kk, v in sizes.items()}
             self.ws = _lib.Workspace(**{kk: b.data_ptr() for kk, b in self.bufs.items()})
@@ -290,7 +290,8 @@ def linear_group_dots(q: QuantizedTensor, x, mode: ExecutionMode):
     st = q.store
     T = t.shape[0]
     L = 1 if mode is ExecutionMode.LOW_PRECISION else 3
-    r = T * L
+    tm = 8 if T <= 8 else 16 if T <= 16 else 32 if T <= 32 else 64   # linear_tmax_bucket
+    r = tm * L
     r_pad = 8 if r <= 8 else -(-r // 16) * 16
     dots = torch.zeros((st.geo.n_pad, st.geo.n_chunks, r_pad), dtype=torch.int32, device="cuda")
     ws = _ws.get(st.n, st.k, st.g)

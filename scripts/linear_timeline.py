@@ -21,7 +21,7 @@ fn = "qs_w4a4_linear" if mode == "w4a4" else "qs_w4a16_linear"
 md = 1 if mode == "w4a4" else 0
 st = _lib.stream_ptr()
 _lib.call(fn, stores[0].store.geo, x.data_ptr(), M, y.data_ptr(), ws, st)
-dbg = torch.zeros(4096, dtype=torch.int64, device="cuda")
+dbg = torch.zeros(8192, dtype=torch.int64, device="cuda")
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 for rep in range(4):
     _lib.call("qs_debug_timeline", dbg.data_ptr() if rep == 3 else None)
@@ -39,6 +39,13 @@ ent, ext = ent[ent > 0], ext[ext > 0]
 t0 = ent.min()
 print(f"event time {e0.elapsed_time(e1)*1e3:.1f} us; CTAs {len(ent)}; entry spread {ent.max()-t0} ns; "
       f"exit min {ext.min()-t0} max {ext.max()-t0} ns; median dur {np.median(ext-ent):.0f} ns")
+fd = d[3072:3072 + 148] - t0
+fx = d[3584:3584 + 148] - t0
+ex = d[2048:2048 + 148] - t0
+order = np.argsort(ex)
+print("slowest CTAs (cta, first_data, last_segment_fixup, exit):", [(int(c), int(fd[c]), int(fx[c]), int(ex[c])) for c in order[-8:]])
+print("fastest CTAs:", [(int(c), int(fd[c]), int(fx[c]), int(ex[c])) for c in order[:4]])
+print("first-data percentiles (ns):", np.percentile(fd, [0, 50, 90, 100]).astype(int))
 print(" i  prod_issue  unpack_done  mma_issued  epi_done   (ns from first CTA entry)")
 for i in range(64):
     if d[i] == 0:

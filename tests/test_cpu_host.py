@@ -60,7 +60,7 @@ def test_workspace_sizes_7b():
                    rope_len=576)
     s = _lib.WorkspaceSizes()
     _lib.call("qs_workspace_size", m, 64, s)
-    assert s.img == 86 * 192 * 128 and s.counters == (250 + 1) * 4
+    assert s.img == 86 * 192 * 128 and s.counters == (4096 + 2) * 4
 
 
 def test_model_config_validation_mirrors_reference():
