@@ -95,14 +95,22 @@ namespace {
 
 // Launch a linear whose operand comes from a.pk: either fused into the linear's
 // pre-phase (grid barrier) or as a separate act_pack launch overlapped via PDL.
-cudaError_t launch_linear_packed(int L, LinearArgs& a, cudaStream_t st) {
+cudaError_t launch_linear_packed(int L, LinearArgs& a, cudaStream_t st, int32_t tag = -1) {
+  const int32_t mode_bits = 16 * (L == 1 ? 1 : 0);
+  cudaError_t e = cudaSuccess;
   if (fuse_pack_enabled()) {
-    return launch_linear(L, a, st);
+    a.fuse_pack = 1;
+  } else {
+    a.fuse_pack = 0;
+    prof_mark(st, mode_bits + 5, true);  // kind 5: operand pack
+    e = launch_act_pack(L, a.pk, st);
+    prof_mark(st, 0, false);
+    if (e != cudaSuccess) return e;
   }
-  a.fuse_pack = 0;
-  cudaError_t e = launch_act_pack(L, a.pk, st);
-  if (e != cudaSuccess) return e;
-  return launch_linear(L, a, st);
+  if (tag >= 0) prof_mark(st, tag, true);
+  e = launch_linear(L, a, st);
+  if (tag >= 0) prof_mark(st, 0, false);
+  return e;
 }
 
 int status(cudaError_t e) {
@@ -453,9 +461,7 @@ int qs_forward(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const qs_
     a.block_table = m->block_table;
     a.bt_ld = m->bt_ld;
     a.page = m->page;
-    prof_mark(st, mode * 16 + 0, true);
-    if ((e = launch_linear_packed(L, a, st)) != cudaSuccess) return status(e);
-    prof_mark(st, 0, false);
+    if ((e = launch_linear_packed(L, a, st, mode * 16 + 0)) != cudaSuccess) return status(e);
     // attention (model.py:293-330), split-KV partials
     AttnArgs at{};
     at.q = ws->q;
@@ -481,7 +487,9 @@ int qs_forward(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const qs_
     at.part_o = ws->att_o;
     at.part_ml = ws->att_ml;
     at.cmax = att_cmax;
+    prof_mark(st, mode * 16 + 6, true);  // kind 6: attention
     if ((e = launch_attention(at, b->n_blk, st)) != cudaSuccess) return status(e);
+    prof_mark(st, 0, false);
     // o_proj + residual (model.py:332); its fused pre-phase merges the attention chunks
     a = linear_args(ly.o, T, L, ws, kOpResidual, ws->x, d);
     a.pk = pack_args(ly.o, ws->attn, d, T, ws, L);
@@ -491,23 +499,17 @@ int qs_forward(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const qs_
     a.pk.att_hd = hd;
     a.pk.att_cmax = att_cmax;
     a.pk.att_chunk = attention_chunk_len();
-    prof_mark(st, mode * 16 + 1, true);
-    if ((e = launch_linear_packed(L, a, st)) != cudaSuccess) return status(e);
-    prof_mark(st, 0, false);
+    if ((e = launch_linear_packed(L, a, st, mode * 16 + 1)) != cudaSuccess) return status(e);
     // gate|up on rmsnorm(x), epilogue silu(gate) * up (model.py:333-335)
     a = linear_args(ly.gate_up, T, L, ws, kOpSiluMul, ws->h, ff);
     a.pk = pack_args(ly.gate_up, ws->x, d, T, ws, L);
     a.pk.rms_w = ly.ffn_norm;
     a.pk.eps = m->norm_eps;
-    prof_mark(st, mode * 16 + 2, true);
-    if ((e = launch_linear_packed(L, a, st)) != cudaSuccess) return status(e);
-    prof_mark(st, 0, false);
+    if ((e = launch_linear_packed(L, a, st, mode * 16 + 2)) != cudaSuccess) return status(e);
     // down_proj + residual (model.py:336)
     a = linear_args(ly.down, T, L, ws, kOpResidual, ws->x, d);
     a.pk = pack_args(ly.down, ws->h, ff, T, ws, L);
-    prof_mark(st, mode * 16 + 3, true);
-    if ((e = launch_linear_packed(L, a, st)) != cudaSuccess) return status(e);
-    prof_mark(st, 0, false);
+    if ((e = launch_linear_packed(L, a, st, mode * 16 + 3)) != cudaSuccess) return status(e);
   }
   // final norm + lm_head + argmax (model.py:342-344, numerics.py:81-86)
   LinearArgs a = linear_args(m->lm_head, T, L, ws, kOpLogits, logits, m->vocab);
@@ -515,9 +517,7 @@ int qs_forward(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const qs_
   a.pk.rms_w = m->final_norm;
   a.pk.eps = m->norm_eps;
   a.argmax_out = argmax;
-  prof_mark(st, mode * 16 + 4, true);
-  e = launch_linear_packed(L, a, st);
-  prof_mark(st, 0, false);
+  e = launch_linear_packed(L, a, st, mode * 16 + 4);
   return status(e);
 }
 

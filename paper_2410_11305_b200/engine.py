@@ -126,7 +126,7 @@ class DecodeEngine:
     def launches_per_step(self) -> int:
         """Kernels one step launches (for the bench's gpu_launches claim)."""
         L = self.cfg.n_layers
-        fwd = 5 * L + 1
+        fwd = 9 * L + 2  # per layer: 4 packs, 4 linears, attention; + final pack + lm_head
         if self.algorithm == "qspec":
             return self.gamma * (1 + fwd * len(self.draft_batches)) + 1 + fwd * len(self.verify_batches) + 1
         return 2 + fwd * len(self.draft_batches)
