@@ -152,6 +152,7 @@ def run_decode(model, a, batch: int, algorithm: str, prompts: np.ndarray, steps:
            "acceptance_rate": (na / nd) if nd else None, "launches_per_step": eng.launches_per_step(),
            "clocks": ck}
     if profile:
+        out["ctx_mean"] = float(eng.t["committed"].float().mean().item())
         out["profile"] = eng.profile_step()
     del eng
     torch.cuda.empty_cache()
@@ -191,51 +192,65 @@ def run_e2e(model, a, batch: int, prompts: np.ndarray) -> dict:
             "cycles": cycles, "tokens": toks, "wall_s": wall}
 
 
-def linear_roofline(model, a, prof: list, batch: int) -> dict:
-    """Dominant kernel (the tensor-core linear): algorithmic bytes per launch / event-timed duration.
+def forward_bytes(model, T: int, ctx_sum: float) -> float:
+    """Algorithmic HBM bytes of one forward over T tokens.
 
-    Per launch: N*K/2 packed codes + 4*N*K/g scales + 4*T*K fp32 activations read + 4*T*N outputs
-    written.  Durations come from event pairs recorded around every launch of one
-    replayed step (qs_profile_*), on the stream the kernels run on.
+    Per linear: N*K/2 packed codes + 4*N*K/g scales + 4*T*K activations in + 4*T*N out;
+    attention: fp32 K and V rows of every context position of every token's sequence
+    (ctx_sum = sum over the forward's query blocks of their context length), all layers.
     """
+    cfg = model.config
     lw = model.layers[0]
-    stores = [lw.qkv, lw.o, lw.gate_up, lw.down, model.lm_head.store]
+    tot = 0.0
+    for st, outw in ((lw.qkv, lw.qkv.n), (lw.o, lw.o.n), (lw.gate_up, lw.gate_up.n // 2), (lw.down, lw.down.n)):
+        tot += cfg.n_layers * (st.n * st.k / 2 + 4 * st.n * st.k / st.g + 4 * T * st.k + 4 * T * outw)
+    h = model.lm_head.store
+    tot += h.n * h.k / 2 + 4 * h.n * h.k / h.g + 4 * T * h.k + 4 * T * h.n
+    tot += ctx_sum * cfg.n_layers * cfg.n_kv_heads * cfg.head_dim * 2 * 4
+    return tot
+
+
+def linear_roofline(model, a, prof: list, batch: int, ctx_mean: float) -> dict:
+    """Dominant kernel (forward_mk_kernel: one launch per forward): algorithmic bytes per
+    launch / event-timed launch duration, on the stream the kernel runs on.
+
+    prof = [(ms, tag)] from qs_profile_* event pairs around every forward launch of one
+    replayed step (tag = mode*16 + 7; mode 1 = W4A4 draft, 0 = W4A16 verify).
+    """
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-    tot_b = tot_ms = 0.0
-    kinds, other = {}, {}
-    names = ["qkv", "o", "gate_up", "down", "lm_head", "pack", "attention"]
-    step_ms = 0.0
+    kinds = {}
+    tot_b = tot_ms = step_ms = 0.0
     for ms, tag in prof:
         mode, kind = tag // 16, tag % 16
         step_ms += ms
-        key = ("draft" if mode == 1 else "verify") + "." + names[kind]
-        if kind >= 5:
-            d = other.setdefault(key, [0, 0.0])
-            d[0] += 1
-            d[1] += ms
+        if kind != 7:
             continue
-        T = batch if mode == 1 else batch * (a.gamma + 1)
-        st = stores[kind]
-        outw = st.n // 2 if kind == 2 else st.n
-        byts = st.n * st.k / 2 + 4 * st.n * st.k / st.g + 4 * T * st.k + 4 * T * outw
-        tot_b += byts
-        tot_ms += ms
+        draft = mode == 1
+        T = batch if draft else batch * (a.gamma + 1)
+        # context per query block: the sequence's committed length (+ this pass's rows)
+        ctx = ctx_mean + (1 if draft else a.gamma + 1)
+        byts = forward_bytes(model, T, batch * ctx)
+        key = "draft_forward" if draft else "verify_forward"
         d = kinds.setdefault(key, [0, 0.0, 0.0])
         d[0] += 1
         d[1] += ms
         d[2] += byts
+        tot_b += byts
+        tot_ms += ms
     achieved = tot_b / (tot_ms / 1e3) / 1e9
     peak = peaks["hbm_gbs"]
-    per = {k: {"launches": v[0], "avg_us": round(1e3 * v[1] / v[0], 2), "GBps": round(v[2] / (v[1] / 1e3) / 1e9, 1)}
+    per = {k: {"launches": v[0], "avg_us": round(1e3 * v[1] / v[0], 2), "MB_per_launch": round(v[2] / v[0] / 1e6, 1),
+               "GBps": round(v[2] / (v[1] / 1e3) / 1e9, 1), "frac": round(v[2] / (v[1] / 1e3) / 1e9 / peak, 4)}
            for k, v in kinds.items()}
-    per.update({k: {"launches": v[0], "avg_us": round(1e3 * v[1] / v[0], 2)} for k, v in other.items()})
-    n_lin = sum(v[0] for v in kinds.values())
+    n = sum(v[0] for v in kinds.values())
     return {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
             "frac": round(achieved / peak, 4), "traffic": None,
-            "kernel": "linear_tc_kernel (tcgen05 kind::i8), all launches of one replayed step",
-            "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)", "launches": n_lin,
-            "avg_launch_us": round(1e3 * tot_ms / max(1, n_lin), 2),
-            "linear_share_of_step": round(tot_ms / step_ms, 3) if step_ms else None,
+            "kernel": "forward_mk_kernel (persistent forward: tcgen05 kind::i8 linears + packs + attention)",
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)", "launches": n,
+            "avg_launch_us": round(1e3 * tot_ms / max(1, n), 2),
+            "bytes_per_launch_def": "sum over linears (N*K/2 + 4NK/g + 4TK + 4TN) + fp32 K,V of every context "
+                                    "position of every query block, all layers",
+            "share_of_step": round(tot_ms / step_ms, 3) if step_ms else None,
             "per_kind": per}
 
 
@@ -361,7 +376,7 @@ def main() -> None:
                                  "ms_per_cycle": round(q["ms"] / q["steps"], 3),
                                  "ms_per_ar_step": round(r["ms"] / r["steps"], 3)}
     e2e = run_e2e(model, a, a.batch, prompts)
-    roof = linear_roofline(model, a, main_q["profile"], a.batch)
+    roof = linear_roofline(model, a, main_q["profile"], a.batch, main_q["ctx_mean"])
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu:
         cpu = cpu_reference(a, main_q["acceptance_rate"])

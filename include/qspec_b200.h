@@ -15,6 +15,7 @@
  *                                           quant.py:229-245 fake_quantize_activations
  *   qs_w4a4_linear / qs_w4a16_linear     <- quant.py:248-261 qlinear_forward (LOW / HIGH)
  *   qs_forward                           <- model.py:255-348 forward
+ *   qs_forward_mk                        <- model.py:255-348 forward (one persistent launch)
  *   qs_draft_prep / qs_verify_prep /
  *   qs_accept / qs_ar_prep / qs_ar_commit <- specdec.py:103-176, 258-335 (+ model.py:211-229 kv_commit)
  */
@@ -157,6 +158,12 @@ int qs_profile_read(float* ms, int32_t* tags, int32_t max_out, int32_t* n_out);
 /* ------------------------------------------------------------------ step */
 int qs_forward(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const qs_workspace_t* ws, float* logits,
                int32_t* argmax, void* stream);
+/* Same forward, same results bit for bit, as ONE persistent kernel (forward_mk.cu):
+ * weights stream continuously while device counters order the phases.  The
+ * first call for a given (model, batch, workspace, mode) builds and uploads the
+ * phase program (synchronous); later calls -- and graph captures -- only launch. */
+int qs_forward_mk(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const qs_workspace_t* ws, float* logits,
+                  int32_t* argmax, void* stream);
 
 /* --------------------------------------------------------------- control */
 int qs_draft_prep(const qs_seq_t* s, int32_t step, void* stream);

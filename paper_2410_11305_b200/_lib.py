@@ -84,6 +84,7 @@ _SIGS = {
     "qs_profile_reset": ([], C.c_int),
     "qs_profile_read": ([vp, vp, i32, C.POINTER(i32)], C.c_int),
     "qs_forward": ([C.POINTER(Model), C.POINTER(Batch), i32, C.POINTER(Workspace), vp, vp, vp], C.c_int),
+    "qs_forward_mk": ([C.POINTER(Model), C.POINTER(Batch), i32, C.POINTER(Workspace), vp, vp, vp], C.c_int),
     "qs_draft_prep": ([C.POINTER(Seq), i32, vp], C.c_int),
     "qs_verify_prep": ([C.POINTER(Seq), vp], C.c_int),
     "qs_accept": ([C.POINTER(Seq), vp], C.c_int),

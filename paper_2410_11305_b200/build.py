@@ -43,7 +43,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
         obj = os.path.join(BUILD, os.path.basename(src)[:-3] + ".o")
         objs.append(obj)
         if force or _stale(obj, [src] + headers):
-            extra = []
+            extra = os.environ.get("QS_NVCC_EXTRA", "").split()
             jobs.append([NVCC, *ARCH, *FLAGS, *extra, "-c", src, "-o", obj])
 
     def run(cmd: list[str]) -> None:

@@ -145,6 +145,26 @@ struct AttnArgs {
   int ldo;
 };
 
+// Persistent forward kernel program (forward_mk.cu): one entry per phase.
+enum MkKind : int { kMkPack = 0, kMkLin = 1, kMkAttn = 2 };
+struct MkPhase {
+  int kind;
+  int dep;        // phase whose completion this phase waits for (-1: none)
+  int dep_count;  // completion count of that phase
+  int n_blk;      // kMkAttn: query blocks
+  LinearArgs lin;
+  PackArgs pk;
+  AttnArgs at;
+};
+struct MkArgs {
+  const MkPhase* prog;
+  int n_phases;
+  const int* lin_phase;  // phase index of each linear, in program order
+  int n_lin;
+  int* cnt;              // [n_phases + 1] completion counters: zero on entry, reset on exit
+  unsigned long long* dbg;  // optional [n_phases][4] %globaltimer timeline of CTA 0 (NULL: off)
+};
+
 struct QuantWArgs {
   // source: LCG (src == nullptr) or fp32 row-major [rows, cols]
   const float* src;

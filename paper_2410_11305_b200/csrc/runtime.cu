@@ -6,6 +6,10 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
 
 #include "../../include/qspec_b200.h"
 #include "qs_common.cuh"
@@ -27,6 +31,10 @@ cudaError_t launch_repack_ref(const uint8_t* ref_codes, const float* ref_scales,
                               int row_stride, cudaStream_t st);
 
 cudaError_t launch_control(int op, const SeqState& s, int j, cudaStream_t st);
+cudaError_t launch_forward_mk(int L, int T, const MkArgs& g, int n_cta, cudaStream_t st);
+int mk_tmax_bucket(int T, int L);
+int mk_attn_chunk_len();
+cudaError_t launch_mk_attn_debug(const MkPhase* prog, int phase, unsigned long long* td, int n_cta, cudaStream_t st);
 }  // namespace qs
 
 using namespace qs;
@@ -49,6 +57,7 @@ bool pdl_enabled() {
 }
 }  // namespace qs
 
+static unsigned long long* g_dbg = nullptr;
 namespace {
 
 constexpr int kMaxT = 64;
@@ -400,7 +409,6 @@ int qs_w4a16_linear(const qs_qweight_t* w, const float* x, int32_t T, float* y, 
   return run_linear(w, x, T, y, ws, 3, kOpStore, nullptr, (cudaStream_t)stream);
 }
 
-static unsigned long long* g_dbg = nullptr;
 int qs_debug_timeline(uint64_t* buf) {
   g_dbg = reinterpret_cast<unsigned long long*>(buf);
   return QS_OK;
@@ -521,6 +529,192 @@ int qs_forward(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const qs_
   return status(e);
 }
 
+}  // extern "C"
+
+// ---------------------------------------------------------------- persistent forward
+// The phase program of one forward (model.py:255-348) for the persistent kernel
+// (forward_mk.cu): the same arguments qs_forward passes to its per-step launches,
+// plus the dependency edges between phases.  Programs are cached by content
+// (they hold only pointers and shapes), so a CUDA-graph capture replays a
+// program built -- and copied to the device -- during the warm-up call.
+namespace {
+struct MkProgram {
+  MkPhase* d_prog = nullptr;
+  int* d_lin = nullptr;
+  int* d_cnt = nullptr;
+  int n_phases = 0, n_lin = 0;
+};
+std::map<std::string, MkProgram> g_mk_cache;
+
+int mk_supported(const qs_model_t* m, const qs_batch_t* b) {
+  const int hd = m->d_model / m->n_heads;
+  if (hd % 4 != 0 || hd > 128) return 0;
+  if (attention_chunk_len() != mk_attn_chunk_len()) return 0;
+  if (m->page % 8 != 0) return 0;  // attention loads 8-key batches from one page
+  (void)b;
+  return 1;
+}
+}  // namespace
+
+extern "C" int qs_forward_mk(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const qs_workspace_t* ws,
+                             float* logits, int32_t* argmax, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  const int T = b->T;
+  if (T < 1 || T > kMaxT) return QS_ERR_SHAPE;
+  const int L = mode == QS_MODE_LOW ? 1 : 3;
+  const int d = m->d_model, H = m->n_heads, KV = m->n_kv_heads, hd = d / H, ff = m->d_ff;
+  const int hpk = H / KV;
+  if (b->blk_qmax * hpk > 64 || hd % 4 != 0) return QS_ERR_SHAPE;
+  if (b->ctx_cap > m->rope_len) return QS_ERR_OVERFLOW;
+  if (!mk_supported(m, b)) return qs_forward(m, b, mode, ws, logits, argmax, stream);
+  const int att_cmax = attention_chunks(m->rope_len);
+  const int grid = num_sms();
+  std::vector<MkPhase> prog;
+  std::vector<int> lin;
+  auto add = [&](const MkPhase& p) {
+    prog.push_back(p);
+    if (p.kind == kMkLin) lin.push_back((int)prog.size() - 1);
+    return (int)prog.size() - 1;
+  };
+  auto pack_phase = [&](const PackArgs& pk, int dep, int dep_count) {
+    MkPhase p;
+    memset(&p, 0, sizeof(p));
+    p.kind = kMkPack;
+    p.dep = dep;
+    p.dep_count = dep_count;
+    p.pk = pk;
+    return add(p);
+  };
+  auto lin_phase = [&](const LinearArgs& a, int dep) {
+    MkPhase p;
+    memset(&p, 0, sizeof(p));
+    p.kind = kMkLin;
+    p.dep = dep;
+    p.dep_count = grid;
+    p.lin = a;
+    p.lin.pk = PackArgs{};
+    return add(p);
+  };
+  int prev = -1, prev_count = 0;
+  for (int li = 0; li < m->n_layers; ++li) {
+    const qs_layer_t& ly = m->layers[li];
+    PackArgs pk = pack_args(ly.qkv, ws->x, d, T, ws, L);
+    pk.rms_w = ly.attn_norm;
+    pk.eps = m->norm_eps;
+    if (li == 0) {
+      pk.gather_ids = b->tokens;
+      pk.emb = m->tok_emb;
+      pk.x_out = ws->x;
+    }
+    int p = pack_phase(pk, prev, prev_count);
+    LinearArgs a = linear_args(ly.qkv, T, L, ws, kOpQkvRope, ws->q, H * hd);
+    a.pos = b->positions;
+    a.slot = b->slots;
+    a.rope_cos = m->rope_cos;
+    a.rope_sin = m->rope_sin;
+    a.hd = hd;
+    a.n_q = H * hd;
+    a.n_k = KV * hd;
+    a.n_kv_heads = KV;
+    a.kcache = ly.k_cache;
+    a.vcache = ly.v_cache;
+    a.block_table = m->block_table;
+    a.bt_ld = m->bt_ld;
+    a.page = m->page;
+    const int p_qkv = lin_phase(a, p);
+    MkPhase at;
+    memset(&at, 0, sizeof(at));
+    at.kind = kMkAttn;
+    at.dep = p_qkv;
+    at.dep_count = ly.qkv.n_tiles;
+    at.n_blk = b->n_blk;
+    AttnArgs& t = at.at;
+    t.q = ws->q;
+    t.ldq = H * hd;
+    t.kcache = ly.k_cache;
+    t.vcache = ly.v_cache;
+    t.block_table = m->block_table;
+    t.bt_ld = m->bt_ld;
+    t.page = m->page;
+    t.pos = b->positions;
+    t.slot = b->slots;
+    t.blk_tok0 = b->blk_tok0;
+    t.blk_ntok = b->blk_ntok;
+    t.H = H;
+    t.KV = KV;
+    t.hd = hd;
+    t.hpk = hpk;
+    t.inv_sqrt_hd = 1.0f / sqrtf((float)hd);
+    t.qmax = b->blk_qmax;
+    t.ctx_cap = b->ctx_cap;
+    t.out = ws->attn;
+    t.ldo = d;
+    t.part_o = ws->att_o;
+    t.part_ml = ws->att_ml;
+    t.cmax = att_cmax;
+    const int p_att = add(at);
+    pk = pack_args(ly.o, ws->attn, d, T, ws, L);
+    pk.att_o = ws->att_o;
+    pk.att_ml = ws->att_ml;
+    pk.att_pos = b->positions;
+    pk.att_hd = hd;
+    pk.att_cmax = att_cmax;
+    pk.att_chunk = attention_chunk_len();
+    p = pack_phase(pk, p_att, grid);
+    const int p_o = lin_phase(linear_args(ly.o, T, L, ws, kOpResidual, ws->x, d), p);
+    pk = pack_args(ly.gate_up, ws->x, d, T, ws, L);
+    pk.rms_w = ly.ffn_norm;
+    pk.eps = m->norm_eps;
+    p = pack_phase(pk, p_o, ly.o.n_tiles);
+    const int p_gu = lin_phase(linear_args(ly.gate_up, T, L, ws, kOpSiluMul, ws->h, ff), p);
+    p = pack_phase(pack_args(ly.down, ws->h, ff, T, ws, L), p_gu, ly.gate_up.n_tiles);
+    prev = lin_phase(linear_args(ly.down, T, L, ws, kOpResidual, ws->x, d), p);
+    prev_count = ly.down.n_tiles;
+  }
+  PackArgs pk = pack_args(m->lm_head, ws->x, d, T, ws, L);
+  pk.rms_w = m->final_norm;
+  pk.eps = m->norm_eps;
+  const int p = pack_phase(pk, prev, prev_count);
+  LinearArgs a = linear_args(m->lm_head, T, L, ws, kOpLogits, logits, m->vocab);
+  a.argmax_out = argmax;
+  lin_phase(a, p);
+
+  // the persistent kernel's image height (its own token buckets)
+  const int r_pad = img_rows(mk_tmax_bucket(T, L), L);
+  for (MkPhase& ph : prog) {
+    if (ph.kind == kMkPack) ph.pk.r_pad = r_pad;
+    if (ph.kind == kMkLin) ph.lin.r_pad = r_pad;
+  }
+  std::string key(reinterpret_cast<const char*>(prog.data()), prog.size() * sizeof(MkPhase));
+  key.append(reinterpret_cast<const char*>(&grid), sizeof(grid));
+  auto itp = g_mk_cache.find(key);
+  if (itp == g_mk_cache.end()) {
+    MkProgram mp;
+    mp.n_phases = (int)prog.size();
+    mp.n_lin = (int)lin.size();
+    cudaError_t e;
+    if ((e = cudaMalloc(&mp.d_prog, prog.size() * sizeof(MkPhase))) != cudaSuccess) return status(e);
+    if ((e = cudaMalloc(&mp.d_lin, lin.size() * sizeof(int))) != cudaSuccess) return status(e);
+    if ((e = cudaMalloc(&mp.d_cnt, (prog.size() + 1) * sizeof(int))) != cudaSuccess) return status(e);
+    if ((e = cudaMemcpy(mp.d_prog, prog.data(), prog.size() * sizeof(MkPhase), cudaMemcpyHostToDevice)) !=
+        cudaSuccess)
+      return status(e);
+    if ((e = cudaMemcpy(mp.d_lin, lin.data(), lin.size() * sizeof(int), cudaMemcpyHostToDevice)) != cudaSuccess)
+      return status(e);
+    if ((e = cudaMemset(mp.d_cnt, 0, (prog.size() + 1) * sizeof(int))) != cudaSuccess) return status(e);
+    if ((e = cudaDeviceSynchronize()) != cudaSuccess) return status(e);
+    itp = g_mk_cache.emplace(key, mp).first;
+  }
+  const MkProgram& mp = itp->second;
+  MkArgs g{mp.d_prog, mp.n_phases, mp.d_lin, mp.n_lin, mp.d_cnt, g_dbg};
+  if (getenv("QS_MK_ATTN_ONLY")) return status(launch_mk_attn_debug(mp.d_prog, 2, g_dbg, grid, st));
+  prof_mark(st, mode * 16 + 7, true);  // kind 7: whole persistent forward
+  cudaError_t e = launch_forward_mk(L, T, g, grid, st);
+  prof_mark(st, 0, false);
+  return status(e);
+}
+
+extern "C" {
 int qs_draft_prep(const qs_seq_t* s, int32_t step, void* stream) {
   return status(launch_control(0, seq_state(s), step, (cudaStream_t)stream));
 }
