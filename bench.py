@@ -211,45 +211,57 @@ def forward_bytes(model, T: int, ctx_sum: float) -> float:
 
 
 def linear_roofline(model, a, prof: list, batch: int, ctx_mean: float) -> dict:
-    """Dominant kernel (forward_mk_kernel: one launch per forward): algorithmic bytes per
-    launch / event-timed launch duration, on the stream the kernel runs on.
+    """Dominant kernel's roofline: algorithmic bytes per launch / event-timed launch duration
+    (events on the stream the kernels run on; qs_profile_* brackets every launch of one
+    replayed step, tag = mode*16 + kind, mode 1 = W4A4 draft, 0 = W4A16 verify).
 
-    prof = [(ms, tag)] from qs_profile_* event pairs around every forward launch of one
-    replayed step (tag = mode*16 + 7; mode 1 = W4A4 draft, 0 = W4A16 verify).
+    Per-step path (default): the dominant kernel is linear_tc_kernel; bytes per launch =
+    N*K/2 codes + 4*N*K/g scales + 4*T*K activations + 4*T*N outputs.
+    Persistent path (QSPEC_PERSISTENT=1): one forward_mk_kernel launch per forward; bytes =
+    the same linear terms for every linear of the forward + fp32 K,V of every context row.
     """
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-    kinds = {}
+    peak = peaks["hbm_gbs"]
+    lw = model.layers[0]
+    stores = [lw.qkv, lw.o, lw.gate_up, lw.down, model.lm_head.store]
+    names = ["qkv", "o", "gate_up", "down", "lm_head", "pack", "attention", "forward"]
+    kinds, other = {}, {}
     tot_b = tot_ms = step_ms = 0.0
+    persistent = any(tag % 16 == 7 for _, tag in prof)
     for ms, tag in prof:
         mode, kind = tag // 16, tag % 16
         step_ms += ms
-        if kind != 7:
-            continue
         draft = mode == 1
         T = batch if draft else batch * (a.gamma + 1)
-        # context per query block: the sequence's committed length (+ this pass's rows)
-        ctx = ctx_mean + (1 if draft else a.gamma + 1)
-        byts = forward_bytes(model, T, batch * ctx)
-        key = "draft_forward" if draft else "verify_forward"
+        key = ("draft" if draft else "verify") + "." + names[kind]
+        if kind == 7:
+            byts = forward_bytes(model, T, batch * (ctx_mean + (1 if draft else a.gamma + 1)))
+        elif kind < 5 and not persistent:
+            st = stores[kind]
+            outw = st.n // 2 if kind == 2 else st.n
+            byts = st.n * st.k / 2 + 4 * st.n * st.k / st.g + 4 * T * st.k + 4 * T * outw
+        else:
+            d = other.setdefault(key, [0, 0.0])
+            d[0] += 1
+            d[1] += ms
+            continue
         d = kinds.setdefault(key, [0, 0.0, 0.0])
         d[0] += 1
         d[1] += ms
         d[2] += byts
         tot_b += byts
         tot_ms += ms
-    achieved = tot_b / (tot_ms / 1e3) / 1e9
-    peak = peaks["hbm_gbs"]
-    per = {k: {"launches": v[0], "avg_us": round(1e3 * v[1] / v[0], 2), "MB_per_launch": round(v[2] / v[0] / 1e6, 1),
-               "GBps": round(v[2] / (v[1] / 1e3) / 1e9, 1), "frac": round(v[2] / (v[1] / 1e3) / 1e9 / peak, 4)}
-           for k, v in kinds.items()}
+    achieved = tot_b / (tot_ms / 1e3) / 1e9 if tot_ms else 0.0
+    per = {k: {"launches": v[0], "avg_us": round(1e3 * v[1] / v[0], 2), "MB_per_launch": round(v[2] / v[0] / 1e6, 2),
+               "GBps": round(v[2] / (v[1] / 1e3) / 1e9, 1)} for k, v in kinds.items()}
+    per.update({k: {"launches": v[0], "avg_us": round(1e3 * v[1] / v[0], 2)} for k, v in other.items()})
     n = sum(v[0] for v in kinds.values())
+    kernel = ("forward_mk_kernel (persistent forward)" if persistent
+              else "linear_tc_kernel (tcgen05 kind::i8), all launches of one replayed step")
     return {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-            "frac": round(achieved / peak, 4), "traffic": None,
-            "kernel": "forward_mk_kernel (persistent forward: tcgen05 kind::i8 linears + packs + attention)",
+            "frac": round(achieved / peak, 4), "traffic": None, "kernel": kernel,
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)", "launches": n,
             "avg_launch_us": round(1e3 * tot_ms / max(1, n), 2),
-            "bytes_per_launch_def": "sum over linears (N*K/2 + 4NK/g + 4TK + 4TN) + fp32 K,V of every context "
-                                    "position of every query block, all layers",
             "share_of_step": round(tot_ms / step_ms, 3) if step_ms else None,
             "per_kind": per}
 

@@ -55,10 +55,14 @@ struct MkCfg {
   static constexpr int kActBytes = kRowsMax * 128;
   static constexpr int kWStageBytes = kCPS * kChunkBytes;
   static constexpr int kAStageBytes = kCPS * kActBytes;
-  static constexpr int kASt = kAStageBytes <= 8192 ? 3 : 2;
-  static constexpr int kSSt = 4;
+  // operand (image) and scale rings deep enough that the operand producer can run a
+  // whole linear's images ahead of the MMA once its dependency is met (~48 KB)
+  static constexpr int kASt0 = (48 * 1024) / kAStageBytes;
+  static constexpr int kASt = kASt0 < 2 ? 2 : (kASt0 > 8 ? 8 : kASt0);
+  static constexpr int kSSt = 8;
   static constexpr int kSEntry = kCPS * (128 + TMAX) * 4;
-  static constexpr int kWorkBytes = 4096;  // worker scratch: [0, 2K) logits argmax reduction, [2K, 3K) phase args
+  // worker scratch: [0, 2K) logits argmax reduction, [2K, 3K) phase args, [4K, ..) attention q / scores
+  static constexpr int kWorkBytes = 4096 + (16 * 128 + 16 * 64 + 16 + 16) * 4;
   // 4 control warps + 4 unpack warps + 4 (T <= 8) or 8 worker warps: 384 threads
   // (168 registers each, no spills) for small T, 512 for the wide epilogues.
   static constexpr int kUnpackWarps = TMAX <= 8 ? 8 : 4;  // 2 (1) warps per TMEM lane quadrant
@@ -212,22 +216,25 @@ __device__ __forceinline__ float warp_inv_rms(const PackArgs& a, int t, int lane
   const int K4 = a.K >> 2;
   float part[4] = {0.f, 0.f, 0.f, 0.f};
   for (int base = 0; base < K4; base += 512) {
-    float4 v[4][4];  // every load of the step in flight at once
 #pragma unroll
-    for (int vw = 0; vw < 4; ++vw)
+    for (int vh = 0; vh < 4; vh += 2) {  // 8 loads in flight (no spills)
+      float4 v[2][4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int k4 = base + u * 128 + vw * 32 + lane;
-        v[vw][u] = k4 < K4 ? __ldcg(row4 + k4) : make_float4(0.f, 0.f, 0.f, 0.f);
-      }
+      for (int vw = 0; vw < 2; ++vw)
 #pragma unroll
-    for (int vw = 0; vw < 4; ++vw) {
+        for (int u = 0; u < 4; ++u) {
+          const int k4 = base + u * 128 + (vh + vw) * 32 + lane;
+          v[vw][u] = k4 < K4 ? __ldcg(row4 + k4) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        part[vw] = __fadd_rn(part[vw], __fmul_rn(v[vw][u].x, v[vw][u].x));
-        part[vw] = __fadd_rn(part[vw], __fmul_rn(v[vw][u].y, v[vw][u].y));
-        part[vw] = __fadd_rn(part[vw], __fmul_rn(v[vw][u].z, v[vw][u].z));
-        part[vw] = __fadd_rn(part[vw], __fmul_rn(v[vw][u].w, v[vw][u].w));
+      for (int vw = 0; vw < 2; ++vw) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          part[vh + vw] = __fadd_rn(part[vh + vw], __fmul_rn(v[vw][u].x, v[vw][u].x));
+          part[vh + vw] = __fadd_rn(part[vh + vw], __fmul_rn(v[vw][u].y, v[vw][u].y));
+          part[vh + vw] = __fadd_rn(part[vh + vw], __fmul_rn(v[vw][u].z, v[vw][u].z));
+          part[vh + vw] = __fadd_rn(part[vh + vw], __fmul_rn(v[vw][u].w, v[vw][u].w));
+        }
       }
     }
   }
@@ -255,7 +262,7 @@ constexpr int kMkChunk = 64;
 // Branch-free around every shuffle (selects and predicated loads only): a shuffle
 // the compiler cannot prove converged gets a BRA.DIV + WARPSYNC.COLLECTIVE slow path.
 template <int QG>
-__device__ __noinline__ void attn_warp_item(const AttnArgs& a, int blk, int kvh, int ch, int qg, int lane,
+__device__ __forceinline__ void attn_warp_item(const AttnArgs& a, int blk, int kvh, int ch, int qg, int lane,
                                            unsigned long long* td) {
   constexpr int kKB = 8;  // keys per load batch
   if (td && lane == 0) td[0] = gtimer();
@@ -390,8 +397,132 @@ __device__ __noinline__ void attn_warp_item(const AttnArgs& a, int blk, int kvh,
   }
 }
 
+// CTA-wide split-KV attention partial of (block blk, kv head kvh, key chunk ch): the
+// worker warps share the chunk's 64 keys, exactly as attn_partial_kernel's CTA does
+// (score of key jj by one warp: lane-split dot + xor tree; softmax of query qi by one
+// warp; o_c[qi][d] = sequential fma over keys by one thread) -- bit-identical to it,
+// with each warp's K rows and each thread's V column fetched in one batch.
+constexpr int kMkAttnQ = 16;  // queries (block tokens x GQA group) per CTA item
+template <int NW>
+__device__ __noinline__ void attn_cta_item(const AttnArgs& a, int blk, int kvh, int ch, int et, float* sm,
+                                           unsigned long long* td) {
+  constexpr int NT = NW * 32, KPW = kMkChunk / NW;  // keys per warp
+  const int w = et >> 5, lane = et & 31;
+  if (td && et == 0) td[0] = gtimer();
+  const int ntok = a.blk_ntok[blk];
+  if (ntok <= 0) return;
+  const int tok0 = a.blk_tok0[blk];
+  const int j0 = ch * kMkChunk;
+  int cmax = 0;
+  for (int i = 0; i < ntok; ++i) cmax = max(cmax, a.pos[tok0 + i] + 1);
+  if (j0 >= cmax) return;
+  const int nk = min(kMkChunk, cmax - j0);
+  const int hpk = a.hpk, Q = ntok * hpk, H = a.H, hd = a.hd, page = a.page, KV = a.KV, cmx = a.cmax;
+  const float inv_sqrt_hd = a.inv_sqrt_hd;
+  const float* kcache = a.kcache;
+  const float* vcache = a.vcache;
+  const int* bt = a.block_table + (size_t)a.slot[tok0] * a.bt_ld;
+  float* qv = sm;                       // [Q][hd]
+  float* sc = qv + kMkAttnQ * 128;      // [Q][64]
+  int* ctx_s = reinterpret_cast<int*>(sc + kMkAttnQ * kMkChunk);  // [Q]
+  int* pg_s = ctx_s + kMkAttnQ;                                   // [64 / page] page ids of the chunk
+  const bool dl = lane * 4 < hd;
+  const int dv = et % hd;
+  const int npg = (nk + page - 1) / page;
+  if (et < npg) pg_s[et] = bt[(j0 + et * page) / page];
+  // row offset (floats) of key jj of the chunk
+  auto row = [&](int jj) -> size_t {
+    const int j = j0 + jj;
+    return (((size_t)pg_s[jj / page] * KV + kvh) * page + (j % page)) * hd;
+  };
+  // queries -> smem (cp.async 16 B), contexts
+  for (int e = et; e < Q * (hd >> 2); e += NT) {
+    const int qi = e / (hd >> 2), d4 = e - qi * (hd >> 2);
+    const int i = qi / hpk, h = kvh * hpk + qi % hpk;
+    cp_async16_cg(qv + qi * hd + d4 * 4, a.q + (size_t)(tok0 + i) * a.ldq + (size_t)h * hd + d4 * 4);
+  }
+  if (et < Q) ctx_s[et] = a.pos[tok0 + et / hpk] + 1;
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  named_bar(1, NT);
+  // V rows of the chunk toward L2 now (loaded after the scores): 128-byte lines
+  {
+    const int lpr = (hd * 4 + 127) / 128;
+    for (int l = et; l < nk * lpr; l += NT)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(vcache + row(l / lpr) + (l % lpr) * 32));
+  }
+  if (td && et == 0) td[1] = gtimer();
+  // ---- scores: warp w owns keys jj = w + NW*u (the key -> warp map does not change a score)
+  {
+    float4 kr[KPW];
+#pragma unroll
+    for (int u = 0; u < KPW; ++u) {
+      const int jj = w + NW * u;
+      const float4* src = reinterpret_cast<const float4*>(kcache + row(jj < nk ? jj : 0)) + lane;
+      kr[u] = (jj < nk && dl) ? *src : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int u = 0; u < KPW; ++u) {
+      const int jj = w + NW * u, j = j0 + jj;
+      for (int qi = 0; qi < Q; ++qi) {
+        const float4 q4 = dl ? *reinterpret_cast<const float4*>(qv + qi * hd + lane * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
+        float p = 0.f;
+        p = fmaf(q4.x, kr[u].x, p);
+        p = fmaf(q4.y, kr[u].y, p);
+        p = fmaf(q4.z, kr[u].z, p);
+        p = fmaf(q4.w, kr[u].w, p);
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) p += __shfl_xor_sync(0xffffffffu, p, off);
+        if (lane == 0 && jj < nk) sc[qi * kMkChunk + jj] = (j < ctx_s[qi]) ? p * inv_sqrt_hd : -INFINITY;
+      }
+    }
+  }
+  named_bar(1, NT);
+  if (td && et == 0) td[2] = gtimer();
+  // ---- chunk softmax statistics (warp per query)
+  for (int qi = w; qi < Q; qi += NW) {
+    float* s = sc + qi * kMkChunk;
+    float m = -INFINITY;
+    for (int jj = lane; jj < nk; jj += 32) m = fmaxf(m, s[jj]);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+    float l = 0.f;
+    for (int jj = lane; jj < nk; jj += 32) {
+      const float e = (m == -INFINITY) ? 0.f : expf(s[jj] - m);
+      s[jj] = e;
+      l += e;
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) l += __shfl_xor_sync(0xffffffffu, l, off);
+    if (lane == 0) {
+      const int i = qi / hpk, h = kvh * hpk + qi % hpk;
+      reinterpret_cast<float2*>(a.part_ml)[((size_t)(tok0 + i) * H + h) * cmx + ch] = make_float2(m, l);
+    }
+  }
+  named_bar(1, NT);
+  if (td && et == 0) td[3] = gtimer();
+  // ---- o_c[qi][d] = sum_j p_j v_j[d], keys ascending; thread owns dimension dv
+  if (et < hd * ((NT / hd) < Q ? (NT / hd) : Q)) {
+    const int qstep = NT / hd;  // query stride between the threads sharing dv
+    float vv[kMkChunk];
+#pragma unroll
+    for (int jj = 0; jj < kMkChunk; ++jj) {
+      vv[jj] = jj < nk ? vcache[row(jj) + dv] : 0.f;
+    }
+    for (int qi = et / hd; qi < Q; qi += qstep) {
+      const float* pp = sc + qi * kMkChunk;
+      float acc = 0.f;
+#pragma unroll
+      for (int jj = 0; jj < kMkChunk; ++jj) acc = jj < nk ? fmaf(pp[jj], vv[jj], acc) : acc;
+      const int i = qi / hpk, h = kvh * hpk + qi % hpk;
+      a.part_o[(((size_t)(tok0 + i) * H + h) * cmx + ch) * hd + dv] = acc;
+    }
+  }
+  named_bar(1, NT);  // smem reused by the next item
+  if (td && et == 0) td[4] = gtimer();
+}
+
 template <int L>
-__device__ __noinline__ void pack_warp_item(const PackArgs& pk, int t, int gi, int lane) {
+__device__ __forceinline__ void pack_warp_item(const PackArgs& pk, int t, int gi, int lane) {
   const float inv = pk.rms_w != nullptr ? warp_inv_rms(pk, t, lane) : 1.0f;
   pack_group<L>(pk, t, gi, inv, lane);
 }
@@ -549,7 +680,9 @@ __global__ void __launch_bounds__(MkCfg<L, TMAX>::kThreads, 1) forward_mk_kernel
         if (sdbg && lane == 0 && i < 256) sdbg[6 * 256 + i] = gtimer();
         mk_wait_warp(&tfull[as_], (i / C::kASlots) & 1);
         if (sdbg && lane == 0 && i < 256) sdbg[7 * 256 + i] = gtimer();
+#if !QS_NO_MMA_PROXY_FENCE
         fence_proxy_async_smem();  // cp.async-written image -> tensor-core (async proxy) reads
+#endif
         tc_fence_after();
         const uint64_t bdesc0 = sdesc_sw128(smem_u32(smem + C::kAOff + sa * C::kAStageBytes));
         const uint32_t d0 = tmem + b * CPS * C::kAccCols;
@@ -645,6 +778,7 @@ __global__ void __launch_bounds__(MkCfg<L, TMAX>::kThreads, 1) forward_mk_kernel
     int i = 0;  // global stage counter (same sequence as every other role)
     uint8_t* argbuf = smem + C::kWorkOff + 2048;  // this phase's arguments (smem copy)
     for (int p = 0; p < g.n_phases; ++p) {
+      if (g.dbg != nullptr && et == 0 && p > 0) g.dbg[8192 + (p - 1) * NCTA + c] = gtimer();  // my share of p-1 done
       const MkPhase* php = &prog[p];
       const int kind = __ldg(&php->kind), dep = __ldg(&php->dep), dep_count = __ldg(&php->dep_count);
       {
@@ -672,7 +806,6 @@ __global__ void __launch_bounds__(MkCfg<L, TMAX>::kThreads, 1) forward_mk_kernel
             const int t = it / pk.G, gi = it - t * pk.G;
             pack_warp_item<L>(pk, t, gi, lane);
           }
-          fence_proxy_async_global();  // generic image writes -> bulk-copy reads in other CTAs
         } else {
           const AttnArgs& at = *reinterpret_cast<const AttnArgs*>(argbuf);
           const int qg_size = at.qmax * at.hpk == 1 ? 1 : 4;
@@ -689,31 +822,6 @@ __global__ void __launch_bounds__(MkCfg<L, TMAX>::kThreads, 1) forward_mk_kernel
             const int blk = rem / at.KV;
             unsigned long long* td = nullptr;
             if (sdbg && p < 12 && ew == 0) td = sdbg + 10 * 256 + 8 * ((it - c * C::kEpiWarps) / (NCTA * C::kEpiWarps));
-            if (td) {  // latency probe: 4 rounds of 8 independent row loads from the K cache
-              float acc = 0.f;
-              for (int rnd = 0; rnd < 4; ++rnd) {
-                const unsigned long long t0 = gtimer();
-                float4 v[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u)
-                  v[u] = reinterpret_cast<const float4*>(at.kcache + ((size_t)(rnd * 8 + u) * 37 + (acc == 1.5f)) * 128)[lane];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) acc += v[u].x;
-                if (lane == 0) td[9 + rnd] = gtimer() - t0 + (acc == 7.f);
-              }
-              // ALU probe: 2048 dependent FMAs (4-cycle latency each at full rate)
-              const unsigned long long t0 = gtimer();
-              float x = acc * 1e-30f + 1.0f;
-#pragma unroll 16
-              for (int k = 0; k < 2048; ++k) x = fmaf(x, 0.999f, 1e-7f);
-              if (lane == 0) td[13] = gtimer() - t0 + (x == 7.f);
-              // shuffle probe: 256 dependent xor shuffles
-              const unsigned long long t1 = gtimer();
-              float y = x;
-#pragma unroll 16
-              for (int k = 0; k < 256; ++k) y += __shfl_xor_sync(0xffffffffu, y, k & 31);
-              if (lane == 0) td[14] = gtimer() - t1 + (y == 7.f);
-            }
             if (qg_size == 1)
               attn_warp_item<1>(at, blk, kvh, ch, qg, lane, td);
             else
@@ -721,8 +829,7 @@ __global__ void __launch_bounds__(MkCfg<L, TMAX>::kThreads, 1) forward_mk_kernel
             if (td && lane == 0) td[4] = gtimer();
           }
         }
-        __threadfence();
-        named_bar(1, kEpiT);
+        named_bar(1, kEpiT);  // the release below is cumulative over the CTA's writes
         if (et == 0) red_release_add(&g.cnt[p], 1);
         if (dbg) g.dbg[4 * p + 2] = gtimer();
         continue;
@@ -819,7 +926,6 @@ __global__ void __launch_bounds__(MkCfg<L, TMAX>::kThreads, 1) forward_mk_kernel
                 const int t = (kH * lc + h) * 8 + e;
                 if (t < a.T) __stcg(my + t * kTileN + r, acc[lc * 8 + e]);
               }
-            __threadfence();
             named_bar(1, kEpiT);
             if (et == 0) red_release_add(&a.counters[tile], 1);
 #pragma unroll
@@ -949,7 +1055,6 @@ __global__ void __launch_bounds__(MkCfg<L, TMAX>::kThreads, 1) forward_mk_kernel
           }
         }
         // tile complete: publish (phase count = n_tiles)
-        __threadfence();
         named_bar(1, kEpiT);
         if (et == 0) red_release_add(&g.cnt[p], 1);
         if (dbg) g.dbg[4 * p + 2] = gtimer();
@@ -957,6 +1062,7 @@ __global__ void __launch_bounds__(MkCfg<L, TMAX>::kThreads, 1) forward_mk_kernel
         for (int t = 0; t < kOwn * 8; ++t) acc[t] = 0.f;
       }
     }
+    if (g.dbg != nullptr && et == 0) g.dbg[8192 + (g.n_phases - 1) * NCTA + c] = gtimer();
   }
   tc_fence_before();
   __syncthreads();

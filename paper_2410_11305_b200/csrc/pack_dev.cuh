@@ -35,6 +35,47 @@ __device__ __forceinline__ float pack_load(const PackArgs& a, int t, int k, cons
   return __fdiv_rn(acc, Ls);
 }
 
+// pack_load's attention combine for 4 consecutive elements k..k+3 of one head, with
+// every chunk statistic / partial fetched in batches (same per-element association:
+// max over chunks, then one sequential fma chain over chunks).
+__device__ __forceinline__ float4 merge4(const PackArgs& a, int t, int k) {
+  const int H = a.K / a.att_hd;
+  const int h = k / a.att_hd, d = k - h * a.att_hd;
+  const int nch = (a.att_pos[t] + a.att_chunk) / a.att_chunk;
+  const float2* ml = reinterpret_cast<const float2*>(a.att_ml) + ((size_t)t * H + h) * a.att_cmax;
+  const float* o = a.att_o + (((size_t)t * H + h) * a.att_cmax) * a.att_hd + d;
+  float M = -INFINITY;
+  for (int c0 = 0; c0 < nch; c0 += 8) {
+    float2 mv[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) mv[u] = (c0 + u < nch) ? __ldcg(ml + c0 + u) : make_float2(-INFINITY, 0.f);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) M = (c0 + u < nch) ? fmaxf(M, mv[u].x) : M;
+  }
+  float Ls = 0.f, acc[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int c0 = 0; c0 < nch; c0 += 4) {
+    float2 mv[4];
+    float4 ov[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const bool on = c0 + u < nch;
+      mv[u] = on ? __ldcg(ml + c0 + u) : make_float2(0.f, 0.f);
+      ov[u] = on ? __ldcg(reinterpret_cast<const float4*>(o + (size_t)(c0 + u) * a.att_hd)) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (c0 + u < nch) {
+        const float w = expf(mv[u].x - M);
+        Ls = fmaf(w, mv[u].y, Ls);
+        acc[0] = fmaf(w, ov[u].x, acc[0]);
+        acc[1] = fmaf(w, ov[u].y, acc[1]);
+        acc[2] = fmaf(w, ov[u].z, acc[2]);
+        acc[3] = fmaf(w, ov[u].w, acc[3]);
+      }
+    }
+  }
+  return make_float4(__fdiv_rn(acc[0], Ls), __fdiv_rn(acc[1], Ls), __fdiv_rn(acc[2], Ls), __fdiv_rn(acc[3], Ls));
+}
 
 // 1/sqrt(mean(x^2) + eps) of token t's input row, computed cooperatively by
 // nthreads threads (fixed stride + fixed tree => identical in every CTA that
@@ -81,11 +122,13 @@ __device__ __forceinline__ void pack_group(const PackArgs& a, int t, int gi, flo
   float val[kMaxIter][4];
   float m = 0.f;
   const bool vec = (a.att_o == nullptr) && ((g & 3) == 0);
+  const bool att4 = (a.att_o != nullptr) && ((g & 3) == 0) && ((a.att_hd & 3) == 0);
 #pragma unroll
   for (int it = 0; it < kMaxIter; ++it) {
     const int o0 = it * 128 + lane * 4;
     float4 raw = make_float4(0.f, 0.f, 0.f, 0.f);
     if (vec && o0 < g) raw = *reinterpret_cast<const float4*>(src_row + gi * g + o0);
+    if (att4 && o0 < g) raw = merge4(a, t, gi * g + o0);
     const float rv[4] = {raw.x, raw.y, raw.z, raw.w};
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
@@ -93,7 +136,7 @@ __device__ __forceinline__ void pack_group(const PackArgs& a, int t, int gi, flo
       float v = 0.f;
       if (o < g) {
         const int k = gi * g + o;
-        v = vec ? rv[e] : pack_load(a, t, k, src_row);
+        v = (vec || att4) ? rv[e] : pack_load(a, t, k, src_row);
         if (a.x_out) a.x_out[(size_t)t * K + k] = v;
         if (a.rms_w != nullptr) v = __fmul_rn(__fmul_rn(v, inv), a.rms_w[k]);
         if (a.y_out) a.y_out[(size_t)t * K + k] = v;
@@ -102,8 +145,8 @@ __device__ __forceinline__ void pack_group(const PackArgs& a, int t, int gi, flo
       m = fmaxf(m, fabsf(v));
     }
   }
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+  // group max|x| in one warp reduction: non-negative floats order like their bit patterns
+  m = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(m)));
   float s, mul;
   int e2 = 0;
   if constexpr (L == 1) {

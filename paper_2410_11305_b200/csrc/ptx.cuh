@@ -48,16 +48,15 @@ __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
-// Warp-cooperative wait: one lane polls (with back-off), the warp reconverges.
-// Keeps the SM's barrier unit free for the producer / MMA threads.
+// Warp-wide wait: every lane polls the barrier, so the warp stays converged (a lone
+// polling lane leaves the other 31 spinning in WARPSYNC, which steals issue slots
+// from the warps sharing the SM sub-partition).  backoff_ns > 0 sleeps between polls.
 __device__ __forceinline__ void mbar_wait_warp(uint64_t* bar, uint32_t parity, uint32_t backoff_ns = 32) {
-  if ((threadIdx.x & 31) == 0) {
-    if (backoff_ns == 0) {
-      while (!mbar_try(bar, parity)) {
-      }
-    } else {
-      while (!mbar_try(bar, parity)) __nanosleep(backoff_ns);
+  if (backoff_ns == 0) {
+    while (!mbar_try(bar, parity)) {
     }
+  } else {
+    while (!mbar_try(bar, parity)) __nanosleep(backoff_ns);
   }
   __syncwarp();
 }

@@ -550,8 +550,9 @@ int mk_supported(const qs_model_t* m, const qs_batch_t* b) {
   const int hd = m->d_model / m->n_heads;
   if (hd % 4 != 0 || hd > 128) return 0;
   if (attention_chunk_len() != mk_attn_chunk_len()) return 0;
-  if (m->page % 8 != 0) return 0;  // attention loads 8-key batches from one page
-  (void)b;
+  if (m->page < 8) return 0;                                // <= 8 pages per 64-key chunk
+  if (b->blk_qmax * (m->n_heads / m->n_kv_heads) > 16) return 0;  // queries per attention item
+
   return 1;
 }
 }  // namespace

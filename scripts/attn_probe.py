@@ -10,7 +10,7 @@ from bench import CFG7B
 B = int(sys.argv[1]) if len(sys.argv) > 1 else 1
 cfg = dict(CFG7B, n_layers=2)
 model = Q.random_init(Q.ModelConfig(**cfg), 0)
-eng = DecodeEngine(model, B, gamma=3, algorithm="greedy", use_graphs=False)
+eng = DecodeEngine(model, B, gamma=3, algorithm="greedy", use_graphs=False, persistent=True)
 prompts = np.random.default_rng(42).integers(0, cfg["vocab_size"], size=(B, 128))
 for b in range(B):
     eng.prefill(b, [int(t) for t in prompts[b]], 64)

@@ -12,7 +12,7 @@ algo = sys.argv[2] if len(sys.argv) > 2 else "greedy"
 layers = int(os.environ.get("LAYERS", "32"))
 cfg = dict(CFG7B, n_layers=layers)
 model = Q.random_init(Q.ModelConfig(**cfg), 0)
-eng = DecodeEngine(model, B, gamma=3, algorithm=algo, use_graphs=False)
+eng = DecodeEngine(model, B, gamma=3, algorithm=algo, use_graphs=False, persistent=True)
 prompts = np.random.default_rng(42).integers(0, cfg["vocab_size"], size=(B, 128))
 for b in range(B):
     eng.prefill(b, [int(t) for t in prompts[b]], 64)

@@ -23,14 +23,21 @@ if os.environ.get("DMODEL"):  # shrink the model (TLB / L2 experiments): d, ff s
     cfg.update(d_model=d, n_heads=max(1, d // 128), n_kv_heads=max(1, d // 128), d_ff=int(os.environ.get("DFF", 2 * d)),
                vocab_size=int(os.environ.get("VOCAB", 4096)))
 model = Q.random_init(Q.ModelConfig(**cfg), 0)
-eng = DecodeEngine(model, B, gamma=3, algorithm="greedy", greedy_low=low, use_graphs=False)
+eng = DecodeEngine(model, B, gamma=3, algorithm="greedy", greedy_low=low, use_graphs=False, persistent=True)
 prompts = np.random.default_rng(42).integers(0, cfg["vocab_size"], size=(B, 128))
 for b in range(B):
     eng.prefill(b, [int(t) for t in prompts[b]], 64)
 for _ in range(3):
     eng.step()
 torch.cuda.synchronize()
-dbg = torch.zeros(4 * 512 + 11 * 256, dtype=torch.int64, device="cuda")
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+for _ in range(2):
+    e0.record()
+    eng.step()
+    e1.record()
+    torch.cuda.synchronize()
+print(f"step without instrumentation: {e0.elapsed_time(e1) * 1e3:.1f} us")
+dbg = torch.zeros(8192 + 400 * 148, dtype=torch.int64, device="cuda")
 _lib.call("qs_debug_timeline", dbg.data_ptr())
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record()
@@ -78,3 +85,37 @@ for r in ad[:8]:
 raw = dbg.cpu().numpy()[4 * 512 + 10 * 256: 4 * 512 + 11 * 256].reshape(-1, 8)
 print("in-kernel latency probe rounds (us):", [round(float(x) / 1e3, 2) for x in raw[1, 1:5]])
 print("2048 dependent FMA us:", raw[1, 5] / 1e3, " 256 dependent shfl+add us:", raw[1, 6] / 1e3)
+
+# per-CTA completion of every phase: when the phase is complete (max over CTAs) and the spread
+ct = dbg.cpu().numpy()[8192: 8192 + n * 148].reshape(n, 148).astype(np.float64)
+ct = np.where(ct > 0, (ct - t0) / 1e3, np.nan)
+done = np.nanmax(ct, axis=1)
+first = np.nanmin(ct, axis=1)
+agg2 = {}
+prev = 0.0
+for p in range(n):
+    agg2.setdefault(kinds[p], []).append((done[p] - prev, done[p] - first[p], int(np.nanargmax(ct[p]))))
+    prev = done[p]
+print("phase completion (all CTAs): mean duration from previous phase complete, mean spread first->last CTA, slowest CTAs")
+for k, v in agg2.items():
+    a = np.array([x[:2] for x in v])
+    print(f"  {k:10s} {a[:, 0].mean():8.2f} {a[:, 1].mean():8.2f}   slowest {[x[2] for x in v[:4]]}")
+print("forward total (last phase complete):", done[-1])
+# hop latency: CTA 0 sees phase p's dependency satisfied vs the dependency's last publisher
+hops = {}
+for p in range(1, n):
+    dep_done = done[p - 1]
+    seen = rel[p][1]
+    if not np.isnan(seen) and not np.isnan(dep_done):
+        hops.setdefault(kinds[p], []).append(seen - dep_done)
+print("hop latency (CTA 0 sees dependency - last CTA published it), us:")
+for k, v in hops.items():
+    print(f"  {k:10s} {np.mean(v):7.2f}")
+# work after the hop: CTA 0 phase done - dependency seen
+print("CTA 0 work after dependency seen, us:")
+w = {}
+for p in range(1, n):
+    if not np.isnan(rel[p][1]) and not np.isnan(ct[p][0]):
+        w.setdefault(kinds[p], []).append(ct[p][0] - rel[p][1])
+for k, v in w.items():
+    print(f"  {k:10s} {np.mean(v):7.2f}")
