@@ -17,5 +17,7 @@ from .specdec import (CycleRecord, GenerationConfig, GenerationResult, SequenceE
                       draft_phase, format_cycle_record, format_trace, generate_greedy, generate_qspec, parse_trace,
                       verify_phase)
 from .storage import model_from_float_tensors, random_init
+from .serving import (LatencySplit, RejectedRequest, Request, ServingStats, format_stats, parse_workload,
+                      per_valid_token_latency, run_fcfs)
 
 __version__ = "0.1.0"
