@@ -60,7 +60,7 @@ struct MkCfg {
   static constexpr int kASt0 = (48 * 1024) / kAStageBytes;
   static constexpr int kASt = kASt0 < 2 ? 2 : (kASt0 > 8 ? 8 : kASt0);
   static constexpr int kSSt = 8;
-  static constexpr int kSEntry = kCPS * (128 + TMAX) * 4;
+  static constexpr int kSEntry = kCPS * (128 + (TMAX < 8 ? 8 : TMAX)) * 4;  // ascale rows are a_ld = roundup(T, 8)
   // worker scratch: [0, 2K) logits argmax reduction, [2K, 3K) phase args, [4K, ..) attention q / scores
   static constexpr int kWorkBytes = 4096 + (16 * 128 + 16 * 64 + 16 + 16) * 4;
   // 4 control warps + 4 unpack warps + 4 (T <= 8) or 8 worker warps: 384 threads

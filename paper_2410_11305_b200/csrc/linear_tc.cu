@@ -59,7 +59,7 @@ struct LinCfg {
   static constexpr int kStages = kStages0 > 8 ? 8 : kStages0;
   static_assert(kStages >= 2, "pipeline depth");
   static constexpr int kSStages = kStages + 2;
-  static constexpr int kSEntry = kCPS * (128 + TMAX) * 4;
+  static constexpr int kSEntry = kCPS * (128 + (TMAX < 8 ? 8 : TMAX)) * 4;  // ascale rows are a_ld = roundup(T, 8)
   // 16 warps: 4 control, then unpack and epilogue warps (2 or 1 per TMEM lane
   // quadrant each).  Small T is unpack-bound -> 8 unpack warps; large T is
   // epilogue-bound -> 8 epilogue warps.
@@ -68,7 +68,8 @@ struct LinCfg {
   static constexpr int kEpiHalves = kEpiWarps / 4;
   static constexpr int kUnpackHalves = kUnpackWarps / 4;
   static constexpr int kEpiThreads = kEpiWarps * 32;
-  static constexpr int kOwnChunks = (TMAX / 8 + kEpiHalves - 1) / kEpiHalves;  // token chunks per epilogue warp
+  static constexpr int kTokChunk = TMAX < 8 ? TMAX : 8;  // tokens per epilogue token chunk (T <= 4 buckets: fewer)
+  static constexpr int kOwnChunks = ((TMAX < 8 ? 8 : TMAX) / 8 + kEpiHalves - 1) / kEpiHalves;  // per epilogue warp
   static constexpr int kScaleOff = kStages * kStageBytes;
   static constexpr int kBarOff = kScaleOff + kSStages * kSEntry;
   static constexpr int kNumBars = 3 * kStages + 2 * kASlots + 2 * kAccBufs + 2 * kSStages;
@@ -394,17 +395,21 @@ __global__ void __launch_bounds__(512, 1) linear_tc_kernel(const LinearArgs a) {
         for (int lc = 0; lc < kOwn; ++lc) {
           const int tc = kH * lc + h;
           if (tc * 8 < a.T) {
-            // one TMEM round trip per token chunk for all chunks of the stage
-            uint32_t rr[CPS][8 * L];
+            // one TMEM round trip per token chunk for all chunks of the stage; only the
+            // columns of the chunk's tokens are drained (kCols = tokens x limbs)
+            constexpr int kCols = C::kTokChunk * L;
+            uint32_t rr[CPS][kCols <= 8 ? 8 : (kCols <= 16 ? 16 : 24)];
 #pragma unroll
             for (int q = 0; q < CPS; ++q) {
               if (q < it.nq) {
-                const uint32_t col0 = tmem + lane_base + (b * CPS + q) * C::kAccCols;
-                if constexpr (L == 1) {
-                  tmem_ld8(col0 + tc * 8, *reinterpret_cast<uint32_t(*)[8]>(rr[q]));
+                const uint32_t col0 = tmem + lane_base + (b * CPS + q) * C::kAccCols + tc * 8 * L;
+                if constexpr (kCols <= 8) {
+                  tmem_ld8(col0, *reinterpret_cast<uint32_t(*)[8]>(rr[q]));
+                } else if constexpr (kCols <= 16) {
+                  tmem_ld16(col0, rr[q]);
                 } else {
-                  tmem_ld16(col0 + tc * 24, rr[q]);
-                  tmem_ld8(col0 + tc * 24 + 16, *reinterpret_cast<uint32_t(*)[8]>(rr[q] + 16));
+                  tmem_ld16(col0, rr[q]);
+                  tmem_ld8(col0 + 16, *reinterpret_cast<uint32_t(*)[8]>(rr[q] + 16));
                 }
               }
             }
@@ -417,7 +422,7 @@ __global__ void __launch_bounds__(512, 1) linear_tc_kernel(const LinearArgs a) {
                 const float4 s1 = *reinterpret_cast<const float4*>(asc + tc * 8 + 4);
                 const float as[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
 #pragma unroll
-                for (int e = 0; e < 8; ++e) {
+                for (int e = 0; e < C::kTokChunk; ++e) {
                   float dv;
                   if constexpr (L == 1) {
                     dv = (float)(int32_t)rr[q][e];
@@ -620,10 +625,16 @@ static cudaError_t launch_linear_t(const LinearArgs& a, cudaStream_t st) {
   return launch_k(linear_tc_kernel<L, TMAX>, dim3(a.n_cta), dim3(512), C::kSmemBytes, st, a);
 }
 
-int linear_tmax_bucket(int T) { return T <= 8 ? 8 : T <= 16 ? 16 : T <= 32 ? 32 : 64; }
+// token buckets; the 3-limb (verify / AR) path adds T <= 2 and T <= 4 (6 / 12 image
+// rows -> UMMA N = 8 / 16, a quarter / half of the TMEM drain of the T <= 8 bucket)
+int linear_tmax_bucket(int T, int L) {
+  if (L == 3 && T <= 2) return 2;
+  if (L == 3 && T <= 4) return 4;
+  return T <= 8 ? 8 : T <= 16 ? 16 : T <= 32 ? 32 : 64;
+}
 
 cudaError_t launch_linear(int L, const LinearArgs& a, cudaStream_t st) {
-  const int tm = linear_tmax_bucket(a.T);
+  const int tm = linear_tmax_bucket(a.T, L);
   if (L == 1) {
     switch (tm) {
       case 8: return launch_linear_t<1, 8>(a, st);
@@ -633,6 +644,8 @@ cudaError_t launch_linear(int L, const LinearArgs& a, cudaStream_t st) {
     }
   }
   switch (tm) {
+    case 2: return launch_linear_t<3, 2>(a, st);
+    case 4: return launch_linear_t<3, 4>(a, st);
     case 8: return launch_linear_t<3, 8>(a, st);
     case 16: return launch_linear_t<3, 16>(a, st);
     case 32: return launch_linear_t<3, 32>(a, st);

@@ -16,7 +16,7 @@
 
 namespace qs {
 cudaError_t launch_linear(int L, const LinearArgs& a, cudaStream_t st);
-int linear_tmax_bucket(int T);
+int linear_tmax_bucket(int T, int L);
 cudaError_t launch_act_pack(int L, const PackArgs& a, cudaStream_t st);
 cudaError_t launch_attention(const AttnArgs& a, int n_blk, cudaStream_t st);
 size_t attention_smem_bytes(int qmax, int hpk, int hd, int ctx_cap);
@@ -150,7 +150,7 @@ PackArgs pack_args(const qs_qweight_t& w, const float* x, int ldx, int T, const 
   p.gp = w.gp;
   p.G = w.G;
   p.n_chunks = w.n_chunks;
-  p.r_pad = img_rows(linear_tmax_bucket(T), L);
+  p.r_pad = img_rows(linear_tmax_bucket(T, L), L);
   p.a_ld = round_up(T, 8);
   p.img = ws->img;
   p.ascale = ws->ascale;
@@ -171,7 +171,7 @@ LinearArgs linear_args(const qs_qweight_t& w, int T, int L, const qs_workspace_t
   a.cpg = w.cpg;
   a.n_chunks = w.n_chunks;
   a.T = T;
-  a.r_pad = img_rows(linear_tmax_bucket(T), L);
+  a.r_pad = img_rows(linear_tmax_bucket(T, L), L);
   a.a_ld = round_up(T, 8);
   const int U = w.n_tiles * w.n_chunks;
   a.n_cta = U < num_sms() ? U : num_sms();

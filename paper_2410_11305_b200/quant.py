@@ -290,7 +290,8 @@ def linear_group_dots(q: QuantizedTensor, x, mode: ExecutionMode):
     st = q.store
     T = t.shape[0]
     L = 1 if mode is ExecutionMode.LOW_PRECISION else 3
-    tm = 8 if T <= 8 else 16 if T <= 16 else 32 if T <= 32 else 64   # linear_tmax_bucket
+    # linear_tmax_bucket(T, L) in linear_tc.cu
+    tm = (2 if T <= 2 else 4) if (L == 3 and T <= 4) else 8 if T <= 8 else 16 if T <= 16 else 32 if T <= 32 else 64
     r = tm * L
     r_pad = 8 if r <= 8 else -(-r // 16) * 16
     dots = torch.zeros((st.geo.n_pad, st.geo.n_chunks, r_pad), dtype=torch.int32, device="cuda")

@@ -121,3 +121,18 @@ def test_forward_mk_graph_replay_counters_reset():
         e.run()
     for b in range(2):
         assert eng.result(b).new_tokens == ref.result(b).new_tokens
+
+
+@pytest.mark.parametrize("name", ["spec6", "7b2l"])
+@pytest.mark.parametrize("algorithm", ["qspec", "greedy"])
+def test_engine_persistent_b1(name, algorithm):
+    """B = 1: the smallest token buckets (T = 1 draft / AR, T = 4 verify)."""
+    model = model_of(name)
+    res = []
+    for persistent in (False, True):
+        eng = DecodeEngine(model, 1, gamma=3, max_new_cap=24, algorithm=algorithm, persistent=persistent)
+        eng.prefill(0, [3, 14, 15, 92, 65, 35], 20)
+        eng.run()
+        res.append(eng.result(0))
+    assert res[0].new_tokens == res[1].new_tokens
+    assert np.array_equal(res[0].trace, res[1].trace)

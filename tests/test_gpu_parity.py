@@ -125,7 +125,10 @@ def test_integer_core_exact_high_limbs(n, k, g, T):
 # ----------------------------------------------------------------- fp32 linear vs oracle
 @pytest.mark.parametrize("mode", [LOW, HIGH])
 @pytest.mark.parametrize("n,k,g,T", [(384, 4096, 128, 1), (11008, 4096, 128, 16), (4096, 11008, 128, 64),
-                                     (96, 64, 32, 3), (1024, 256, 128, 80)])
+                                     (96, 64, 32, 3), (1024, 256, 128, 80),
+                                     # T <= 2 / T <= 4 token buckets with multi-chunk stages + stream-K fixups
+                                     (4096, 4096, 128, 1), (4096, 4096, 128, 2), (12288, 4096, 128, 4),
+                                     (4096, 11008, 128, 3)])
 def test_qlinear_vs_oracle(mode, n, k, g, T):
     rng = np.random.default_rng(n * 3 + T)
     w = (rng.standard_normal((n, k)) / np.sqrt(k)).astype(np.float32)
