@@ -63,23 +63,70 @@ __global__ void __launch_bounds__(256) attn_partial_kernel(const AttnArgs a) {
   cp_async_wait_all();
   __syncthreads();
 
-  // ---- scores: warp per key, lanes split the head dimension, all queries
+  // ---- scores: warp per key, lanes split the head dimension, all queries.  Each
+  // warp owns keys jj = warp + nw*u; the (key, query) dot products of a 4-query block
+  // are independent, so their xor trees are interleaved (same per-pair arithmetic:
+  // lane-ordered fma chain, then p += shfl_xor(p, 16..1)).
   const int warp = tid >> 5, lane = tid & 31, nw = blockDim.x >> 5;
-  for (int jj = warp; jj < nk; jj += nw) {
-    const int j = j0 + jj;
-    for (int qi = 0; qi < Q; ++qi) {
-      float p = 0.f;
+  constexpr int kKPW = kAttnChunk / 8;  // keys per warp at 8 warps
+  if (nw == 8) {
+    for (int q0 = 0; q0 < Q; q0 += 4) {
+      float p[kKPW][4];
+#pragma unroll
+      for (int u = 0; u < kKPW; ++u)
+#pragma unroll
+        for (int qq = 0; qq < 4; ++qq) p[u][qq] = 0.f;
       for (int d = lane * 4; d < hd; d += 128) {
-        const float4 k4 = *reinterpret_cast<const float4*>(kt + jj * hd + d);
-        const float4 q4 = *reinterpret_cast<const float4*>(qv + qi * hd + d);
-        p = fmaf(q4.x, k4.x, p);
-        p = fmaf(q4.y, k4.y, p);
-        p = fmaf(q4.z, k4.z, p);
-        p = fmaf(q4.w, k4.w, p);
+#pragma unroll
+        for (int u = 0; u < kKPW; ++u) {
+          const int jj = warp + 8 * u;
+          const float4 k4 = *reinterpret_cast<const float4*>(kt + jj * hd + d);
+#pragma unroll
+          for (int qq = 0; qq < 4; ++qq) {
+            const int qi = q0 + qq < Q ? q0 + qq : Q - 1;
+            const float4 q4 = *reinterpret_cast<const float4*>(qv + qi * hd + d);
+            p[u][qq] = fmaf(q4.x, k4.x, p[u][qq]);
+            p[u][qq] = fmaf(q4.y, k4.y, p[u][qq]);
+            p[u][qq] = fmaf(q4.z, k4.z, p[u][qq]);
+            p[u][qq] = fmaf(q4.w, k4.w, p[u][qq]);
+          }
+        }
       }
 #pragma unroll
-      for (int off = 16; off > 0; off >>= 1) p += __shfl_xor_sync(0xffffffffu, p, off);
-      if (lane == 0) sc[qi * kAttnChunk + jj] = (j < ctx_s[qi]) ? p * a.inv_sqrt_hd : -INFINITY;
+      for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+        for (int u = 0; u < kKPW; ++u)
+#pragma unroll
+          for (int qq = 0; qq < 4; ++qq) p[u][qq] += __shfl_xor_sync(0xffffffffu, p[u][qq], off);
+      if (lane == 0) {
+#pragma unroll
+        for (int u = 0; u < kKPW; ++u) {
+          const int jj = warp + 8 * u, j = j0 + jj;
+#pragma unroll
+          for (int qq = 0; qq < 4; ++qq) {
+            const int qi = q0 + qq;
+            if (jj < nk && qi < Q) sc[qi * kAttnChunk + jj] = (j < ctx_s[qi]) ? p[u][qq] * a.inv_sqrt_hd : -INFINITY;
+          }
+        }
+      }
+    }
+  } else {
+    for (int jj = warp; jj < nk; jj += nw) {
+      const int j = j0 + jj;
+      for (int qi = 0; qi < Q; ++qi) {
+        float p = 0.f;
+        for (int d = lane * 4; d < hd; d += 128) {
+          const float4 k4 = *reinterpret_cast<const float4*>(kt + jj * hd + d);
+          const float4 q4 = *reinterpret_cast<const float4*>(qv + qi * hd + d);
+          p = fmaf(q4.x, k4.x, p);
+          p = fmaf(q4.y, k4.y, p);
+          p = fmaf(q4.z, k4.z, p);
+          p = fmaf(q4.w, k4.w, p);
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) p += __shfl_xor_sync(0xffffffffu, p, off);
+        if (lane == 0) sc[qi * kAttnChunk + jj] = (j < ctx_s[qi]) ? p * a.inv_sqrt_hd : -INFINITY;
+      }
     }
   }
   __syncthreads();
