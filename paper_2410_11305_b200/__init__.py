@@ -16,7 +16,8 @@ from .quant import (ExecutionMode, QuantizedTensor, activation_quant_calls, dequ
 from .specdec import (CycleRecord, GenerationConfig, GenerationResult, SequenceEngine, TokenSource, accept_greedy,
                       draft_phase, format_cycle_record, format_trace, generate_greedy, generate_qspec, parse_trace,
                       verify_phase)
-from .storage import model_from_float_tensors, random_init
+from .storage import (config_from_text, config_to_text, load_checkpoint, model_from_float_tensors, random_init,
+                      read_checkpoint, save_checkpoint)
 from .serving import (LatencySplit, RejectedRequest, Request, ServingStats, format_stats, parse_workload,
                       per_valid_token_latency, run_fcfs)
 

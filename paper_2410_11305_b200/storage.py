@@ -114,3 +114,201 @@ def model_from_float_tensors(cfg: ModelConfig, tensors: dict) -> TransformerMode
     torch.cuda.synchronize()
     final = dev(tensors["final_norm"])
     return TransformerModel(cfg, emb, layers, final, QuantizedTensor(cfg.vocab_size, cfg.d_model, g, lm))
+
+
+# ---------------------------------------------------------------------------
+# QSPC checkpoints (storage.py:1-28 format, 300-422 save / load)
+# ---------------------------------------------------------------------------
+
+MAGIC = b"QSPC"
+FORMAT_VERSION = 1
+_F32, _I4 = 0, 1
+HEADER_FIELDS = ("n_layers", "d_model", "n_heads", "n_kv_heads", "d_ff", "vocab_size", "max_seq_len", "rope_theta",
+                 "norm_eps", "group_size")
+_FLOATS = {"rope_theta", "norm_eps"}
+_PROJS = ("q_proj", "k_proj", "v_proj", "o_proj", "gate_proj", "up_proj", "down_proj")
+
+
+def config_to_text(cfg: ModelConfig) -> str:
+    """storage.py:189-194: key=value lines, fixed order, floats by repr."""
+    return "".join(f"{f}={getattr(cfg, f)!r}\n" if f in _FLOATS else f"{f}={getattr(cfg, f)}\n"
+                   for f in HEADER_FIELDS)
+
+
+def config_from_text(text: str) -> ModelConfig:
+    """storage.py:197-222 (same errors)."""
+    from .errors import CheckpointError, ConfigError
+    vals: dict[str, str] = {}
+    for lineno, raw in enumerate(text.splitlines(), start=1):
+        line = raw.strip()
+        if not line or line.startswith("#"):
+            continue
+        if "=" not in line:
+            raise CheckpointError(f"header line {lineno}: expected key=value, got {line!r}")
+        k, v = line.split("=", 1)
+        vals[k.strip()] = v.strip()
+    missing = [f for f in HEADER_FIELDS if f not in vals]
+    if missing:
+        raise CheckpointError(f"header missing fields: {', '.join(missing)}")
+    extra = [k for k in vals if k not in HEADER_FIELDS]
+    if extra:
+        raise CheckpointError(f"header has unknown fields: {', '.join(extra)}")
+    try:
+        kw = {f: (float(vals[f]) if f in _FLOATS else int(vals[f])) for f in HEADER_FIELDS}
+    except ValueError as exc:
+        raise CheckpointError(f"header value: {exc}") from exc
+    try:
+        return ModelConfig(**kw)
+    except ConfigError as exc:
+        raise CheckpointError(f"header config invalid: {exc}") from exc
+
+
+def _records(model: TransformerModel):
+    """(name, dtype, shape, payload) in the reference's record order (storage.py:317-336)."""
+    def f32(name, t):
+        a = t.detach().cpu().numpy() if hasattr(t, "detach") else np.asarray(t)
+        return (name, _F32, tuple(a.shape), a.astype("<f4").tobytes())
+
+    def quant(name, q):
+        return [(f"{name}.codes", _I4, (q.out_features, q.in_features), q.codes.tobytes()),
+                (f"{name}.scales", _F32, tuple(q.scales.shape), q.scales.astype("<f4").tobytes())]
+
+    out = [f32("token_embedding", model.token_embedding)]
+    for i, lw in enumerate(model.layers):
+        p = f"layers.{i}"
+        out.append(f32(f"{p}.attn_norm", lw.attn_norm))
+        for proj in _PROJS[:4]:
+            out += quant(f"{p}.{proj}", getattr(lw, proj))
+        out.append(f32(f"{p}.ffn_norm", lw.ffn_norm))
+        for proj in _PROJS[4:]:
+            out += quant(f"{p}.{proj}", getattr(lw, proj))
+    out.append(f32("final_norm", model.final_norm))
+    out += quant("lm_head", model.lm_head)
+    return out
+
+
+def save_checkpoint(model: TransformerModel, path: str) -> None:
+    """storage.py:315-349: byte-deterministic QSPC file of a quantized model (device -> reference layout)."""
+    import io
+    import struct
+    recs = _records(model)
+    header = config_to_text(model.config).encode("utf-8")
+    buf = io.BytesIO()
+    buf.write(MAGIC + struct.pack("<II", FORMAT_VERSION, len(header)) + header + struct.pack("<I", len(recs)))
+    for name, dtype, shape, payload in recs:
+        nb = name.encode("utf-8")
+        buf.write(struct.pack("<H", len(nb)) + nb + struct.pack("<BB", dtype, len(shape)))
+        buf.write(b"".join(struct.pack("<I", d) for d in shape) + struct.pack("<Q", len(payload)) + payload)
+    with open(path, "wb") as f:
+        f.write(buf.getvalue())
+
+
+def read_checkpoint(path: str):
+    """Parse a QSPC file: (config, {name: (dtype, shape, payload)}), with the reference's checks."""
+    import struct
+    from .errors import CheckpointError
+
+    with open(path, "rb") as f:
+        data = f.read()
+    pos = 0
+
+    def take(n, what):
+        nonlocal pos
+        if pos + n > len(data):
+            raise CheckpointError(f"truncated checkpoint while reading {what}")
+        b = data[pos:pos + n]
+        pos += n
+        return b
+
+    magic = take(4, "magic")
+    if magic != MAGIC:
+        raise CheckpointError(f"bad magic {magic!r}, expected {MAGIC!r}")
+    (version,) = struct.unpack("<I", take(4, "version"))
+    if version != FORMAT_VERSION:
+        raise CheckpointError(f"unsupported format version {version}")
+    (hlen,) = struct.unpack("<I", take(4, "header length"))
+    cfg = config_from_text(take(hlen, "header").decode("utf-8"))
+    (count,) = struct.unpack("<I", take(4, "record count"))
+    recs: dict = {}
+    for _ in range(count):
+        (nl,) = struct.unpack("<H", take(2, "record name length"))
+        name = take(nl, "record name").decode("utf-8")
+        dtype, ndim = struct.unpack("<BB", take(2, f"record '{name}' dtype"))
+        shape = tuple(struct.unpack("<I", take(4, f"record '{name}' dims"))[0] for _ in range(ndim))
+        (plen,) = struct.unpack("<Q", take(8, f"record '{name}' payload length"))
+        payload = take(plen, f"record '{name}' payload")
+        n_el = int(np.prod(shape)) if shape else 1
+        if dtype == _F32:
+            want = 4 * n_el
+        elif dtype == _I4:
+            want = (n_el + 1) // 2
+        else:
+            raise CheckpointError(f"record '{name}': unknown dtype code {dtype}")
+        if len(payload) != want:
+            raise CheckpointError(f"record '{name}': payload is {len(payload)} bytes, expected {want} "
+                                  f"for shape {shape}")
+        if name in recs:
+            raise CheckpointError(f"record '{name}': duplicated")
+        recs[name] = (dtype, shape, payload)
+    return cfg, recs
+
+
+def load_checkpoint(path: str) -> TransformerModel:
+    """storage.py:352-422: a reference QSPC checkpoint into the device layout (qs_repack_ref), bit-exact."""
+    import torch
+    from .errors import CheckpointError
+    cfg, recs = read_checkpoint(path)
+    _lib.require_cuda()
+    hd, g = cfg.head_dim, cfg.group_size
+
+    def take_f32(name, shape):
+        if name not in recs:
+            raise CheckpointError(f"record '{name}': missing")
+        dtype, rshape, payload = recs.pop(name)
+        if dtype != _F32 or rshape != shape:
+            raise CheckpointError(f"record '{name}': expected f32 {shape}, found dtype={dtype} shape={rshape}")
+        return torch.from_numpy(np.frombuffer(payload, dtype="<f4").astype(np.float32).reshape(shape).copy())
+
+    def take_quant(name, n, k):
+        cname = f"{name}.codes"
+        if cname not in recs:
+            if name in recs:
+                raise CheckpointError(f"record '{name}': stored as f32 (unquantized checkpoint); "
+                                      f"run the quantize step first")
+            raise CheckpointError(f"record '{cname}': missing")
+        dtype, shape, payload = recs.pop(cname)
+        if dtype != _I4 or shape != (n, k):
+            raise CheckpointError(f"record '{cname}': expected i4-packed ({n}, {k}), found dtype={dtype} "
+                                  f"shape={shape}")
+        codes = torch.from_numpy(np.frombuffer(payload, dtype=np.uint8).copy()).cuda()
+        scales = take_f32(f"{name}.scales", (n, k // g)).cuda()
+        return codes, scales
+
+    layers, lm, emb = _empty_model(cfg)
+    emb.copy_(take_f32("token_embedding", (cfg.vocab_size, cfg.d_model)))
+    st = _lib.stream_ptr()
+    keep = []
+    dims = {"q_proj": (cfg.n_heads * hd, cfg.d_model), "k_proj": (cfg.n_kv_heads * hd, cfg.d_model),
+            "v_proj": (cfg.n_kv_heads * hd, cfg.d_model), "o_proj": (cfg.d_model, cfg.d_model),
+            "gate_proj": (cfg.d_ff, cfg.d_model), "up_proj": (cfg.d_ff, cfg.d_model),
+            "down_proj": (cfg.d_model, cfg.d_ff)}
+    for i, lw in enumerate(layers):
+        p = f"layers.{i}"
+        lw.attn_norm.copy_(take_f32(f"{p}.attn_norm", (cfg.d_model,)))
+        lw.ffn_norm.copy_(take_f32(f"{p}.ffn_norm", (cfg.d_model,)))
+        for proj in _PROJS:
+            n, k = dims[proj]
+            codes, scales = take_quant(f"{p}.{proj}", n, k)
+            keep += [codes, scales]
+            store, off, stride = _placement(cfg, lw, proj)
+            _lib.call("qs_repack_ref", codes.data_ptr(), scales.data_ptr(), n, k, g, store.codes.data_ptr(),
+                      store.scales.data_ptr(), store.geo.n_pad, off, stride, st)
+    final = take_f32("final_norm", (cfg.d_model,)).cuda()
+    codes, scales = take_quant("lm_head", cfg.vocab_size, cfg.d_model)
+    keep += [codes, scales]
+    _lib.call("qs_repack_ref", codes.data_ptr(), scales.data_ptr(), cfg.vocab_size, cfg.d_model, g,
+              lm.codes.data_ptr(), lm.scales.data_ptr(), lm.geo.n_pad, 0, 1, st)
+    if recs:
+        raise CheckpointError(f"unexpected records: {', '.join(sorted(recs))}")
+    torch.cuda.synchronize()
+    return TransformerModel(cfg, emb, layers, final, QuantizedTensor(cfg.vocab_size, cfg.d_model, g, lm))
