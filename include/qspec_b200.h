@@ -16,6 +16,7 @@
  *   qs_w4a4_linear / qs_w4a16_linear     <- quant.py:248-261 qlinear_forward (LOW / HIGH)
  *   qs_forward                           <- model.py:255-348 forward
  *   qs_forward_mk                        <- model.py:255-348 forward (one persistent launch)
+ *   qs_forward_tp                        <- model.py:255-348 forward, one tensor-parallel shard
  *   qs_draft_prep / qs_verify_prep /
  *   qs_accept / qs_ar_prep / qs_ar_commit <- specdec.py:103-176, 258-335 (+ model.py:211-229 kv_commit)
  */
@@ -164,6 +165,17 @@ int qs_forward(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const qs_
  * phase program (synchronous); later calls -- and graph captures -- only launch. */
 int qs_forward_mk(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const qs_workspace_t* ws, float* logits,
                   int32_t* argmax, void* stream);
+
+/* Tensor-parallel forward (config 3, 13B TP 2/4/8): the model struct holds ONE
+ * rank's shard -- q/k/v and gate/up column-split (n_heads, n_kv_heads, d_ff are
+ * the rank's), o_proj and down_proj row-split along K (group-aligned), embedding,
+ * norms and lm_head replicated.  After each row-split linear the partial [T, d]
+ * sum is handed to `allreduce(ptr, count, stream, user)` (e.g. an NCCL all-reduce
+ * enqueued on `stream`), then added into the residual stream: one all-reduce per
+ * block half, 2 per layer.  Returns the hook's failure as QS_ERR_CUDA. */
+typedef int (*qs_allreduce_fn)(float* ptr, int64_t count, void* stream, void* user);
+int qs_forward_tp(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const qs_workspace_t* ws, float* logits,
+                  int32_t* argmax, int32_t world, qs_allreduce_fn allreduce, void* user, void* stream);
 
 /* --------------------------------------------------------------- control */
 int qs_draft_prep(const qs_seq_t* s, int32_t step, void* stream);

@@ -22,6 +22,9 @@ i32, u64, i64, f32 = C.c_int32, C.c_uint64, C.c_int64, C.c_float
 vp = C.c_void_p
 
 
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p)
+
+
 class QWeight(C.Structure):
     _fields_ = [("codes", vp), ("scales", vp)] + [
         (n, i32) for n in ("n", "k", "g", "n_pad", "n_tiles", "G", "gp", "cpg", "n_chunks")]
@@ -85,6 +88,8 @@ _SIGS = {
     "qs_profile_read": ([vp, vp, i32, C.POINTER(i32)], C.c_int),
     "qs_forward": ([C.POINTER(Model), C.POINTER(Batch), i32, C.POINTER(Workspace), vp, vp, vp], C.c_int),
     "qs_forward_mk": ([C.POINTER(Model), C.POINTER(Batch), i32, C.POINTER(Workspace), vp, vp, vp], C.c_int),
+    "qs_forward_tp": ([C.POINTER(Model), C.POINTER(Batch), i32, C.POINTER(Workspace), vp, vp, i32, vp, vp, vp],
+                      C.c_int),
     "qs_draft_prep": ([C.POINTER(Seq), i32, vp], C.c_int),
     "qs_verify_prep": ([C.POINTER(Seq), vp], C.c_int),
     "qs_accept": ([C.POINTER(Seq), vp], C.c_int),

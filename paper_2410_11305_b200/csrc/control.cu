@@ -144,3 +144,17 @@ cudaError_t launch_control(int op, const SeqState& s, int j, cudaStream_t st) {
 }
 
 }  // namespace qs
+
+namespace qs {
+// x += y elementwise (tensor-parallel residual: y = the all-reduced partial of a
+// row-split o_proj / down_proj).  Same fp32 add as the kOpResidual epilogue.
+__global__ void add_rows_kernel(float* __restrict__ x, const float* __restrict__ y, int n) {
+  pdl_launch_dependents();
+  pdl_wait();
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) x[i] = __fadd_rn(x[i], y[i]);
+}
+cudaError_t launch_add_rows(float* x, const float* y, int n, cudaStream_t st) {
+  return launch_k(add_rows_kernel, dim3((n + 255) / 256), dim3(256), 0, st, x, y, n);
+}
+}  // namespace qs

@@ -31,6 +31,7 @@ cudaError_t launch_repack_ref(const uint8_t* ref_codes, const float* ref_scales,
                               int row_stride, cudaStream_t st);
 
 cudaError_t launch_control(int op, const SeqState& s, int j, cudaStream_t st);
+cudaError_t launch_add_rows(float* x, const float* y, int n, cudaStream_t st);
 cudaError_t launch_forward_mk(int L, int T, const MkArgs& g, int n_cta, cudaStream_t st);
 int mk_tmax_bucket(int T, int L);
 int mk_attn_chunk_len();
@@ -430,13 +431,31 @@ int qs_linear_group_dots(const qs_qweight_t* w, const float* x, int32_t T, int32
   return run_linear(w, x, T, nullptr, ws, mode == QS_MODE_LOW ? 1 : 3, kOpDump, dots, (cudaStream_t)stream);
 }
 
-int qs_forward(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const qs_workspace_t* ws, float* logits,
-               int32_t* argmax, void* stream) {
-  cudaStream_t st = (cudaStream_t)stream;
+}  // extern "C"
+
+namespace {
+struct TpHooks {
+  int world;
+  qs_allreduce_fn fn;
+  void* user;
+};
+int forward_impl(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const qs_workspace_t* ws, float* logits,
+                 int32_t* argmax, cudaStream_t st, const TpHooks* tp) {
   const int T = b->T;
   if (T < 1 || T > kMaxT) return QS_ERR_SHAPE;
   const int L = mode == QS_MODE_LOW ? 1 : 3;
-  const int d = m->d_model, H = m->n_heads, KV = m->n_kv_heads, hd = d / H, ff = m->d_ff;
+  const int world = tp ? tp->world : 1;
+  const int d = m->d_model, H = m->n_heads, KV = m->n_kv_heads, hd = d / (H * world), ff = m->d_ff;
+  // tensor parallel: o_proj / down_proj are row-split, so their outputs are partial
+  // sums -> store into ws->attn, all-reduce (caller's hook, e.g. NCCL on this
+  // stream), then add into the residual stream
+  const int res_op = tp ? kOpStore : kOpResidual;
+  float* res_out = tp ? ws->attn : ws->x;
+  auto reduce_into_x = [&]() -> int {
+    int rc = tp->fn(ws->attn, (int64_t)T * d, st, tp->user);
+    if (rc != 0) return QS_ERR_CUDA;
+    return status(launch_add_rows(ws->x, ws->attn, T * d, st));
+  };
   const int hpk = H / KV;
   if (b->blk_qmax * hpk > 64 || hd % 4 != 0) return QS_ERR_SHAPE;
   if (b->ctx_cap > m->rope_len) return QS_ERR_OVERFLOW;
@@ -499,8 +518,8 @@ int qs_forward(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const qs_
     if ((e = launch_attention(at, b->n_blk, st)) != cudaSuccess) return status(e);
     prof_mark(st, 0, false);
     // o_proj + residual (model.py:332); its fused pre-phase merges the attention chunks
-    a = linear_args(ly.o, T, L, ws, kOpResidual, ws->x, d);
-    a.pk = pack_args(ly.o, ws->attn, d, T, ws, L);
+    a = linear_args(ly.o, T, L, ws, res_op, res_out, d);
+    a.pk = pack_args(ly.o, ws->attn, ly.o.k, T, ws, L);
     a.pk.att_o = ws->att_o;
     a.pk.att_ml = ws->att_ml;
     a.pk.att_pos = b->positions;
@@ -508,6 +527,10 @@ int qs_forward(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const qs_
     a.pk.att_cmax = att_cmax;
     a.pk.att_chunk = attention_chunk_len();
     if ((e = launch_linear_packed(L, a, st, mode * 16 + 1)) != cudaSuccess) return status(e);
+    if (tp) {
+      const int rc = reduce_into_x();
+      if (rc) return rc;
+    }
     // gate|up on rmsnorm(x), epilogue silu(gate) * up (model.py:333-335)
     a = linear_args(ly.gate_up, T, L, ws, kOpSiluMul, ws->h, ff);
     a.pk = pack_args(ly.gate_up, ws->x, d, T, ws, L);
@@ -515,9 +538,13 @@ int qs_forward(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const qs_
     a.pk.eps = m->norm_eps;
     if ((e = launch_linear_packed(L, a, st, mode * 16 + 2)) != cudaSuccess) return status(e);
     // down_proj + residual (model.py:336)
-    a = linear_args(ly.down, T, L, ws, kOpResidual, ws->x, d);
+    a = linear_args(ly.down, T, L, ws, res_op, res_out, d);
     a.pk = pack_args(ly.down, ws->h, ff, T, ws, L);
     if ((e = launch_linear_packed(L, a, st, mode * 16 + 3)) != cudaSuccess) return status(e);
+    if (tp) {
+      const int rc = reduce_into_x();
+      if (rc) return rc;
+    }
   }
   // final norm + lm_head + argmax (model.py:342-344, numerics.py:81-86)
   LinearArgs a = linear_args(m->lm_head, T, L, ws, kOpLogits, logits, m->vocab);
@@ -527,6 +554,21 @@ int qs_forward(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const qs_
   a.argmax_out = argmax;
   e = launch_linear_packed(L, a, st, mode * 16 + 4);
   return status(e);
+}
+}  // namespace
+
+extern "C" {
+int qs_forward(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const qs_workspace_t* ws, float* logits,
+               int32_t* argmax, void* stream) {
+  return forward_impl(m, b, mode, ws, logits, argmax, (cudaStream_t)stream, nullptr);
+}
+
+int qs_forward_tp(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const qs_workspace_t* ws, float* logits,
+                  int32_t* argmax, int32_t world, qs_allreduce_fn allreduce, void* user, void* stream) {
+  if (world < 1 || !allreduce || m->n_heads % m->n_kv_heads != 0) return QS_ERR_CONFIG;
+  if (m->d_model % (m->n_heads * world) != 0) return QS_ERR_CONFIG;
+  TpHooks tp{world, allreduce, user};
+  return forward_impl(m, b, mode, ws, logits, argmax, (cudaStream_t)stream, &tp);
 }
 
 }  // extern "C"
