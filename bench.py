@@ -151,6 +151,10 @@ def run_decode(model, a, batch: int, algorithm: str, prompts: np.ndarray, steps:
     out = {"ms": ms, "tokens": tokens, "steps": steps, "tok_s": tokens / (ms / 1e3),
            "acceptance_rate": (na / nd) if nd else None, "launches_per_step": eng.launches_per_step(),
            "clocks": ck}
+    # per-cycle accept lengths of every slot (trace[b][cycle][1]) for the cost model
+    ncyc = eng.t["n_cycles"].cpu().numpy()
+    tr = eng.t["trace"].reshape(batch, -1, 4).cpu().numpy()
+    out["accept_lens"] = [int(tr[b, c, 1]) for b in range(batch) for c in range(min(int(ncyc[b]), tr.shape[1]))]
     if profile:
         out["ctx_mean"] = float(eng.t["committed"].float().mean().item())
         out["profile"] = eng.profile_step()
@@ -388,6 +392,14 @@ def main() -> None:
                                  "ms_per_cycle": round(q["ms"] / q["steps"], 3),
                                  "ms_per_ar_step": round(r["ms"] / r["steps"], 3)}
     e2e = run_e2e(model, a, a.batch, prompts)
+    # reference cost model (costmodel.py:237-257) fed with a MEASURED latency profile
+    from paper_2410_11305_b200.costmodel import AcceptanceModel, analytic_speedup, measure_profile
+    prof = measure_profile(model, [a.batch], ns=(1, 2, a.gamma + 1), ctx=a.prompt + a.new // 4)
+    pred = analytic_speedup(prof, AcceptanceModel.from_trace(main_q["accept_lens"], a.gamma), a.gamma, a.batch)
+    cost_model = {"profile_ms": {"draft": float(prof.draft[a.batch]),
+                                 "verify": {str(n): round(float(c), 4) for n, c in prof.verify[a.batch]}},
+                  "predicted_speedup_vs_ar": round(pred.speedup, 4), "predicted_tokens_per_cycle":
+                  round(pred.tokens_per_cycle, 3), "acceptance_model": "empirical accept-length distribution of the timed run (device traces)"}
     roof = linear_roofline(model, a, main_q["profile"], a.batch, main_q["ctx_mean"])
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu:
@@ -412,6 +424,7 @@ def main() -> None:
         "roofline": roof,
         "cpu_baseline": cpu,
         "e2e": {k: (round(v, 2) if isinstance(v, float) else v) for k, v in e2e.items()},
+        "cost_model": cost_model,
         "gpu_launches": int(main_q["launches_per_step"] * a.steps),
         "clocks": main_q["clocks"],
         "init_s": round(init_s, 2),
