@@ -850,6 +850,7 @@ __global__ void __launch_bounds__(MkCfg<L, TMAX>::kThreads, 1) forward_mk_kernel
         mk_wait_warp(&accfull[b], (i / C::kAccBufs) & 1);
         tc_fence_after();
         const float* se = sring + ss * (C::kSEntry / 4);
+        bool released = false;  // accumulator buffer b handed back to the MMA
         {
           float sw[CPS];
 #pragma unroll
@@ -877,6 +878,13 @@ __global__ void __launch_bounds__(MkCfg<L, TMAX>::kThreads, 1) forward_mk_kernel
                 }
               }
               tmem_wait_ld();
+              // last TMEM read of this stage by this warp: release the buffer before the math
+              if (qb + kQB >= CPS && (lc == kOwn - 1 || (kH * (lc + 1) + h) * 8 >= a.T)) {
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&accempty[b]);
+                released = true;
+              }
 #pragma unroll
               for (int qq = 0; qq < kQB; ++qq) {
                 const int q = qb + qq;
@@ -905,7 +913,7 @@ __global__ void __launch_bounds__(MkCfg<L, TMAX>::kThreads, 1) forward_mk_kernel
         tc_fence_before();
         __syncwarp();
         if (lane == 0) {
-          mbar_arrive(&accempty[b]);
+          if (!released) mbar_arrive(&accempty[b]);
           mbar_arrive(&sempty[ss]);
           if (sdbg && et == 0 && i < 256) sdbg[4 * 256 + i] = gtimer();
         }

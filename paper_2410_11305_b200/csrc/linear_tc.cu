@@ -374,6 +374,7 @@ __global__ void __launch_bounds__(512, 1) linear_tc_kernel(const LinearArgs a) {
       tc_fence_after();
       if (dbg0 && i < 64 && et == 0) a.dbg[10 * 64 + i] = gtimer();
       const float* se = sring + ss * (C::kSEntry / 4);
+      bool released = false;  // accumulator buffer b handed back to the MMA
       if (a.op == kOpDump) {
         if (h == 0) {
           for (int q = 0; q < it.nq; ++q) {
@@ -414,6 +415,14 @@ __global__ void __launch_bounds__(512, 1) linear_tc_kernel(const LinearArgs a) {
               }
             }
             tmem_wait_ld();
+            // every accumulator column this warp reads is in registers: hand the TMEM
+            // buffer back to the MMA now, before the scale-accumulate math
+            if (lc == kOwn - 1 || (kH * (lc + 1) + h) * 8 >= a.T) {
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&accempty[b]);
+              released = true;
+            }
 #pragma unroll
             for (int q = 0; q < CPS; ++q) {
               if (q < it.nq) {
@@ -442,7 +451,7 @@ __global__ void __launch_bounds__(512, 1) linear_tc_kernel(const LinearArgs a) {
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
-        mbar_arrive(&accempty[b]);
+        if (!released) mbar_arrive(&accempty[b]);
         mbar_arrive(&sempty[ss]);
       }
       if (dbg0 && i < 64 && et == 0) a.dbg[3 * 64 + i] = gtimer();
