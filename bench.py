@@ -262,8 +262,17 @@ def linear_roofline(model, a, prof: list, batch: int, ctx_mean: float) -> dict:
     n = sum(v[0] for v in kinds.values())
     kernel = ("forward_mk_kernel (persistent forward)" if persistent
               else "linear_tc_kernel (tcgen05 kind::i8), all launches of one replayed step")
+    # DRAM traffic of one captured launch of the dominant kernel (committed ncu summary)
+    traffic, traffic_note = None, None
+    tf = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tf) and not persistent:
+        t = json.load(open(tf))
+        traffic = t["dram_bytes_per_launch"]
+        k = per.get(t["per_kind"])
+        traffic_note = {"launch": t["kernel"], "source": t["source"],
+                        "algorithmic_bytes_per_launch": round(k["MB_per_launch"] * 1e6) if k else None}
     return {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-            "frac": round(achieved / peak, 4), "traffic": None, "kernel": kernel,
+            "frac": round(achieved / peak, 4), "traffic": traffic, "traffic_of": traffic_note, "kernel": kernel,
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)", "launches": n,
             "avg_launch_us": round(1e3 * tot_ms / max(1, n), 2),
             "share_of_step": round(tot_ms / step_ms, 3) if step_ms else None,
