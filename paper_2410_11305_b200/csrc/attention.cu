@@ -24,6 +24,54 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
+// Scores of keys jj = warp + 8u (u < KPW) for every query, QB queries at a time:
+// per (key, query) a lane-ordered fma chain then p += shfl_xor(p, 16..1); the
+// independent pairs' trees are interleaved.
+template <int QB, int KPW>
+__device__ __forceinline__ void score_block(const float* kt, const float* qv, float* sc, const int* ctx_s, int hd,
+                                            int Q, int nk, int j0, int warp, int lane, float inv_sqrt_hd) {
+  for (int q0 = 0; q0 < Q; q0 += QB) {
+    float p[KPW][QB];
+#pragma unroll
+    for (int u = 0; u < KPW; ++u)
+#pragma unroll
+      for (int qq = 0; qq < QB; ++qq) p[u][qq] = 0.f;
+    for (int d = lane * 4; d < hd; d += 128) {
+#pragma unroll
+      for (int u = 0; u < KPW; ++u) {
+        const int jj = warp + 8 * u;
+        const float4 k4 = *reinterpret_cast<const float4*>(kt + jj * hd + d);
+#pragma unroll
+        for (int qq = 0; qq < QB; ++qq) {
+          const int qi = q0 + qq < Q ? q0 + qq : Q - 1;
+          const float4 q4 = *reinterpret_cast<const float4*>(qv + qi * hd + d);
+          p[u][qq] = fmaf(q4.x, k4.x, p[u][qq]);
+          p[u][qq] = fmaf(q4.y, k4.y, p[u][qq]);
+          p[u][qq] = fmaf(q4.z, k4.z, p[u][qq]);
+          p[u][qq] = fmaf(q4.w, k4.w, p[u][qq]);
+        }
+      }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+      for (int u = 0; u < KPW; ++u)
+#pragma unroll
+        for (int qq = 0; qq < QB; ++qq) p[u][qq] += __shfl_xor_sync(0xffffffffu, p[u][qq], off);
+    if (lane == 0) {
+#pragma unroll
+      for (int u = 0; u < KPW; ++u) {
+        const int jj = warp + 8 * u, j = j0 + jj;
+#pragma unroll
+        for (int qq = 0; qq < QB; ++qq) {
+          const int qi = q0 + qq;
+          if (jj < nk && qi < Q) sc[qi * kAttnChunk + jj] = (j < ctx_s[qi]) ? p[u][qq] * inv_sqrt_hd : -INFINITY;
+        }
+      }
+    }
+  }
+}
+
 __global__ void __launch_bounds__(256) attn_partial_kernel(const AttnArgs a) {
   extern __shared__ __align__(16) float sm[];
   pdl_launch_dependents();
@@ -70,46 +118,10 @@ __global__ void __launch_bounds__(256) attn_partial_kernel(const AttnArgs a) {
   const int warp = tid >> 5, lane = tid & 31, nw = blockDim.x >> 5;
   constexpr int kKPW = kAttnChunk / 8;  // keys per warp at 8 warps
   if (nw == 8) {
-    for (int q0 = 0; q0 < Q; q0 += 4) {
-      float p[kKPW][4];
-#pragma unroll
-      for (int u = 0; u < kKPW; ++u)
-#pragma unroll
-        for (int qq = 0; qq < 4; ++qq) p[u][qq] = 0.f;
-      for (int d = lane * 4; d < hd; d += 128) {
-#pragma unroll
-        for (int u = 0; u < kKPW; ++u) {
-          const int jj = warp + 8 * u;
-          const float4 k4 = *reinterpret_cast<const float4*>(kt + jj * hd + d);
-#pragma unroll
-          for (int qq = 0; qq < 4; ++qq) {
-            const int qi = q0 + qq < Q ? q0 + qq : Q - 1;
-            const float4 q4 = *reinterpret_cast<const float4*>(qv + qi * hd + d);
-            p[u][qq] = fmaf(q4.x, k4.x, p[u][qq]);
-            p[u][qq] = fmaf(q4.y, k4.y, p[u][qq]);
-            p[u][qq] = fmaf(q4.z, k4.z, p[u][qq]);
-            p[u][qq] = fmaf(q4.w, k4.w, p[u][qq]);
-          }
-        }
-      }
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1)
-#pragma unroll
-        for (int u = 0; u < kKPW; ++u)
-#pragma unroll
-          for (int qq = 0; qq < 4; ++qq) p[u][qq] += __shfl_xor_sync(0xffffffffu, p[u][qq], off);
-      if (lane == 0) {
-#pragma unroll
-        for (int u = 0; u < kKPW; ++u) {
-          const int jj = warp + 8 * u, j = j0 + jj;
-#pragma unroll
-          for (int qq = 0; qq < 4; ++qq) {
-            const int qi = q0 + qq;
-            if (jj < nk && qi < Q) sc[qi * kAttnChunk + jj] = (j < ctx_s[qi]) ? p[u][qq] * a.inv_sqrt_hd : -INFINITY;
-          }
-        }
-      }
-    }
+    if (Q == 1)
+      score_block<1, kKPW>(kt, qv, sc, ctx_s, hd, Q, nk, j0, warp, lane, a.inv_sqrt_hd);
+    else
+      score_block<4, kKPW>(kt, qv, sc, ctx_s, hd, Q, nk, j0, warp, lane, a.inv_sqrt_hd);
   } else {
     for (int jj = warp; jj < nk; jj += nw) {
       const int j = j0 + jj;
