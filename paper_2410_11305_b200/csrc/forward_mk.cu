@@ -680,9 +680,7 @@ __global__ void __launch_bounds__(MkCfg<L, TMAX>::kThreads, 1) forward_mk_kernel
         if (sdbg && lane == 0 && i < 256) sdbg[6 * 256 + i] = gtimer();
         mk_wait_warp(&tfull[as_], (i / C::kASlots) & 1);
         if (sdbg && lane == 0 && i < 256) sdbg[7 * 256 + i] = gtimer();
-#if !QS_NO_MMA_PROXY_FENCE
         fence_proxy_async_smem();  // cp.async-written image -> tensor-core (async proxy) reads
-#endif
         tc_fence_after();
         const uint64_t bdesc0 = sdesc_sw128(smem_u32(smem + C::kAOff + sa * C::kAStageBytes));
         const uint32_t d0 = tmem + b * CPS * C::kAccCols;
@@ -1129,39 +1127,5 @@ cudaError_t launch_forward_mk(int L, int T, const MkArgs& g, int n_cta, cudaStre
 }
 
 int mk_attn_chunk_len() { return kMkChunk; }
-
-// Diagnostic: the attention phase of program entry `phase` alone (same item
-// mapping as the persistent kernel's workers), timed items of block 0 / warp 0.
-__global__ void __launch_bounds__(128) mk_attn_debug_kernel(const MkPhase* prog, int phase, unsigned long long* td) {
-  const MkPhase* php = &prog[phase];
-  __shared__ AttnArgs at_s;
-  if (threadIdx.x == 0) at_s = php->at;
-  __syncthreads();
-  const AttnArgs& at = at_s;
-  const int lane = threadIdx.x & 31, ew = threadIdx.x >> 5, c = blockIdx.x, NCTA = gridDim.x;
-  const int qg_size = at.qmax * at.hpk == 1 ? 1 : 4;
-  const int nqg = (at.qmax * at.hpk + qg_size - 1) / qg_size;
-  const int nch = (at.ctx_cap + kMkChunk - 1) / kMkChunk;
-  const int n_items = php->n_blk * at.KV * nch * nqg;
-  for (int it = c * 4 + ew; it < n_items; it += NCTA * 4) {
-    int rem = it;
-    const int qg = rem % nqg;
-    rem /= nqg;
-    const int ch = rem % nch;
-    rem /= nch;
-    const int kvh = rem % at.KV;
-    const int blk = rem / at.KV;
-    unsigned long long* t = (td && c == 0 && ew == 0) ? td + 8 * ((it - c * 4) / (NCTA * 4)) : nullptr;
-    if (qg_size == 1)
-      attn_warp_item<1>(at, blk, kvh, ch, qg, lane, t);
-    else
-      attn_warp_item<4>(at, blk, kvh, ch, qg, lane, t);
-    if (t && lane == 0) t[4] = gtimer();
-  }
-}
-cudaError_t launch_mk_attn_debug(const MkPhase* prog, int phase, unsigned long long* td, int n_cta, cudaStream_t st) {
-  mk_attn_debug_kernel<<<n_cta, 128, 0, st>>>(prog, phase, td);
-  return cudaGetLastError();
-}
 
 }  // namespace qs

@@ -330,20 +330,11 @@ __global__ void __launch_bounds__(512, 1) linear_tc_kernel(const LinearArgs a) {
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               const int m = jp * 4 + e;
-#if QS_EXP == 2
-              v[m] = ww[e];
-              v[16 + m] = ww[e];
-#else
               v[m] = sext_nib(ww[e] & 0x0F0F0F0Fu);
               v[16 + m] = sext_nib((ww[e] >> 4) & 0x0F0F0F0Fu);
-#endif
             }
           }
-#if QS_EXP == 1
-          if (v[0] == 0x12345678u && v[31] == 0x9abcdef0u) a.dbg[4000] = v[5] + v[17];
-#else
           tmem_st32(tmem + lane_base + C::kAColBase + (b * CPS + q) * 32, v);
-#endif
         }
       }
       tmem_wait_st();

@@ -35,7 +35,6 @@ cudaError_t launch_add_rows(float* x, const float* y, int n, cudaStream_t st);
 cudaError_t launch_forward_mk(int L, int T, const MkArgs& g, int n_cta, cudaStream_t st);
 int mk_tmax_bucket(int T, int L);
 int mk_attn_chunk_len();
-cudaError_t launch_mk_attn_debug(const MkPhase* prog, int phase, unsigned long long* td, int n_cta, cudaStream_t st);
 }  // namespace qs
 
 using namespace qs;
@@ -750,7 +749,6 @@ extern "C" int qs_forward_mk(const qs_model_t* m, const qs_batch_t* b, int32_t m
   }
   const MkProgram& mp = itp->second;
   MkArgs g{mp.d_prog, mp.n_phases, mp.d_lin, mp.n_lin, mp.d_cnt, g_dbg};
-  if (getenv("QS_MK_ATTN_ONLY")) return status(launch_mk_attn_debug(mp.d_prog, 2, g_dbg, grid, st));
   prof_mark(st, mode * 16 + 7, true);  // kind 7: whole persistent forward
   cudaError_t e = launch_forward_mk(L, T, g, grid, st);
   prof_mark(st, 0, false);
