@@ -42,6 +42,9 @@ sys.path.insert(0, ROOT)
 
 CFG7B = dict(n_layers=32, d_model=4096, n_heads=32, n_kv_heads=32, d_ff=11008, vocab_size=32000,
              max_seq_len=512, rope_theta=10000.0, norm_eps=1e-5, group_size=128)
+# BASELINE config 3: Llama-3-8B shape (GQA 32/8, 128k vocab), batch 32 per GPU
+CFG8B = dict(n_layers=32, d_model=4096, n_heads=32, n_kv_heads=8, d_ff=14336, vocab_size=128256,
+             max_seq_len=512, rope_theta=500000.0, norm_eps=1e-5, group_size=128)
 METRIC = "QSpec tokens/s per GPU vs W4A16 autoregressive, 7B-shape; draft accept rate"
 UNIT = "tokens/s"
 
@@ -59,11 +62,13 @@ def parse():
     ap.add_argument("--sweep", default="1,4,16", help="extra batch sizes reported under per_batch")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--small", action="store_true", help="tiny config (smoke / CI)")
+    ap.add_argument("--model", default="7b", choices=["7b", "8b"], help="7b: Llama-2-7B shape (headline); "
+                    "8b: Llama-3-8B shape (BASELINE config 3)")
     return ap.parse_args()
 
 
 def workload_name(a) -> str:
-    shape = "tiny-2L-d256" if a.small else "llama2-7b-shape"
+    shape = "tiny-2L-d256" if a.small else ("llama3-8b-shape" if a.model == "8b" else "llama2-7b-shape")
     return (f"{shape} random-init W4 g128 (LCG seed 0), QSpec gamma={a.gamma} greedy, batch {a.batch}/GPU, "
             f"prompt {a.prompt}, {a.new} new tokens")
 
@@ -72,7 +77,7 @@ def model_cfg(a) -> dict:
     if a.small:
         return dict(n_layers=2, d_model=256, n_heads=4, n_kv_heads=4, d_ff=768, vocab_size=1024,
                     max_seq_len=512, group_size=128)
-    return dict(CFG7B)
+    return dict(CFG8B) if a.model == "8b" else dict(CFG7B)
 
 
 # ----------------------------------------------------------------------------- clocks
@@ -422,7 +427,7 @@ def main() -> None:
         "vs_baseline": None, "dtype": "int8 (tcgen05 kind::i8: int4 codes x int4 / 3x8-bit limb activations, int32 "
                                       "accum, fp32 epilogue)",
         "data": "synthetic (LCG random-init weights, rng(42) prompts)",
-        "config": {"workload": workload_name(a), "model": "llama2-7b-shape W4 g128" if not a.small else "tiny",
+        "config": {"workload": workload_name(a), "model": (("llama3-8b-shape" if a.model == "8b" else "llama2-7b-shape") + " W4 g128") if not a.small else "tiny",
                    "global_batch": a.batch * world, "seq_len": a.prompt + a.new, "gamma": a.gamma,
                    "parallelism": f"replicas x{world} (request-sharded, no collective)",
                    "l2": "weights 3.5 GB >> 126 MB L2: every step streams them from HBM (no flush needed)"},
