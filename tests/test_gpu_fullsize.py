@@ -1,0 +1,60 @@
+"""Size-independent properties at the BASELINE's full size (Llama-2-7B shape, 32 layers),
+where the CPU oracle is too slow to run: the integer cores and batch invariance make
+QSpec tokens EQUAL W4A16 greedy tokens (specdec.py:395-408), a HIGH-precision self
+draft accept everything (test_acceptance.py C4), and the persistent forward equal the
+per-step forward -- at B = 1 / 4 / 16 with ragged prompts."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2410_11305_b200 as Q  # noqa: E402
+from paper_2410_11305_b200.engine import DecodeEngine  # noqa: E402
+
+C7B = dict(n_layers=32, d_model=4096, n_heads=32, n_kv_heads=32, d_ff=11008, vocab_size=32000, max_seq_len=512,
+           group_size=128)
+_m: list = []
+
+
+def model7b():
+    if not _m:
+        _m.append(Q.random_init(Q.ModelConfig(**C7B), 0))
+    return _m[0]
+
+
+def _run(B, algorithm, n_new=12, **kw):
+    m = model7b()
+    rng = np.random.default_rng(42)
+    eng = DecodeEngine(m, B, gamma=3, max_new_cap=n_new + 4, algorithm=algorithm, **kw)
+    for b in range(B):
+        eng.prefill(b, [int(t) for t in rng.integers(0, 32000, 17 + 5 * b)], n_new)
+    eng.run()
+    return [eng.result(b) for b in range(B)]
+
+
+@pytest.mark.parametrize("B", [1, 4, 16])
+def test_7b_qspec_equals_w4a16_greedy(B):
+    q = _run(B, "qspec")
+    g = _run(B, "greedy")
+    for rq, rg in zip(q, g):
+        assert rq.new_tokens == rg.new_tokens
+        assert len(rq.new_tokens) == 12
+
+
+def test_7b_high_self_draft_accepts_everything():
+    r = _run(4, "qspec", draft_low=False)
+    for x in r:
+        assert x.n_drafted > 0 and x.n_accepted == x.n_drafted
+
+
+def test_7b_persistent_equals_per_step():
+    a = _run(4, "qspec", n_new=8, persistent=False)
+    b = _run(4, "qspec", n_new=8, persistent=True)
+    for ra, rb in zip(a, b):
+        assert ra.new_tokens == rb.new_tokens and np.array_equal(ra.trace, rb.trace)
