@@ -18,8 +18,10 @@ def main():
     import paper_2410_11305_b200 as Q
     from paper_2410_11305_b200 import _lib
     from paper_2410_11305_b200.quant import _ws
-    peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
-                                       "MEASURED_PEAKS.json")))["hbm_gbs"]
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    peak = json.load(open(os.path.join(root, "MEASURED_PEAKS.json")))["hbm_gbs"]
+    i8 = os.path.join(root, "profiles", "int8_peak.json")   # scripts/int8_peak.py (cuBLASLt int8)
+    int8_tops = json.load(open(i8))["int8_tops_measured"] if os.path.exists(i8) else None
     out = []
     for shp in a.shapes.split(","):
         n, k = map(int, shp.split("x"))
@@ -30,16 +32,23 @@ def main():
         for M in map(int, a.ms.split(",")):
             x = torch.randn(M, k, device="cuda")
             y = torch.empty(M, n, device="cuda")
+            # the C ABI takes <= 64 tokens per call (qs_linear_max_tokens); larger M runs as
+            # 64-token calls, each streaming the weights again (what qlinear_forward does)
+            chunks = [(m0, min(64, M - m0)) for m0 in range(0, M, 64)]
             for mode, fn in (("w4a4", "qs_w4a4_linear"), ("w4a16", "qs_w4a16_linear")):
                 ws = _ws.get(n, k, 128)
                 st = _lib.stream_ptr()
+                def call(i):
+                    for m0, mm in chunks:
+                        _lib.call(fn, stores[i % copies].store.geo, x[m0:].data_ptr(), mm, y[m0:].data_ptr(), ws, st)
+
                 for i in range(3):
-                    _lib.call(fn, stores[i % copies].store.geo, x.data_ptr(), M, y.data_ptr(), ws, st)
+                    call(i)
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 torch.cuda.synchronize()
                 e0.record()
                 for i in range(a.reps):
-                    _lib.call(fn, stores[i % copies].store.geo, x.data_ptr(), M, y.data_ptr(), ws, st)
+                    call(i)
                 e1.record()
                 torch.cuda.synchronize()
                 us = e0.elapsed_time(e1) * 1e3 / a.reps
@@ -47,7 +56,8 @@ def main():
                 md = 1 if mode == "w4a4" else 0
                 e0.record()
                 for i in range(a.reps):
-                    _lib.call("qs_linear_prepacked", stores[i % copies].store.geo, M, md, y.data_ptr(), ws, st)
+                    for m0, mm in chunks:
+                        _lib.call("qs_linear_prepacked", stores[i % copies].store.geo, mm, md, y[m0:].data_ptr(), ws, st)
                 e1.record()
                 torch.cuda.synchronize()
                 us_lin = e0.elapsed_time(e1) * 1e3 / a.reps
@@ -56,6 +66,8 @@ def main():
                      "GBps_linear_only": round(byts / us_lin / 1e3, 1), "GBps": round(byts / us / 1e3, 1),
                      "frac_hbm": round(byts / us / 1e3 / peak, 3),
                      "TOPS": round(2 * M * n * k * (3 if mode == "w4a16" else 1) / us / 1e6, 2)}
+                if int8_tops:  # tensor-pipe fraction of the int8 MACs the kernel actually issues
+                    r["frac_int8_tensor"] = round(r["TOPS"] / int8_tops, 4)
                 out.append(r)
                 print(json.dumps(r), flush=True)
         del stores
