@@ -26,15 +26,23 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                : "memory");
 }
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity);
+__device__ __forceinline__ unsigned long long gtimer();
+// Spin on an mbarrier phase; a wait that exceeds ~5 s traps (a synchronisation bug
+// surfaces as a launch failure instead of a wedged GPU).
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  uint32_t addr = smem_u32(bar);
-  asm volatile(
-      "{\n\t.reg .pred P1;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-      "@!P1 bra WAIT_%=;\n\t}" ::"r"(addr),
-      "r"(parity)
-      : "memory");
+  uint32_t n = 0;
+  unsigned long long t0 = 0;
+  while (!mbar_try(bar, parity)) {
+    if ((++n & 0xFFFu) == 0) {
+      const unsigned long long t = gtimer();
+      if (t0 == 0) {
+        t0 = t;
+      } else if (t - t0 > 5000000000ull) {
+        __trap();
+      }
+    }
+  }
 }
 
 __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
