@@ -269,9 +269,12 @@ __device__ __forceinline__ void fence_proxy_async_global() {
 __device__ __forceinline__ void grid_barrier_wait(volatile int* gen0_s, int* gbar) {
   if ((threadIdx.x & 31) == 0) {
     int g0;
+    const unsigned long long t0 = gtimer();
     while ((g0 = *gen0_s) < 0) {
+      if (gtimer() - t0 > 5000000000ull) __trap();
     }
     while (ld_acquire(&gbar[1]) == g0) {
+      if (gtimer() - t0 > 5000000000ull) __trap();
     }
     fence_proxy_async_global();
   }

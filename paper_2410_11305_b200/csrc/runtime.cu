@@ -43,7 +43,12 @@ namespace qs {
 bool fuse_pack_enabled() {
   static int on = -1;
   if (on < 0) {
+#if QS_FUSED_PACK
+    const char* e = getenv("QS_FUSED_PACK_ON");  // experiment: operand pack as a pre-phase of the linear
+    on = (e && e[0] == '1') ? 1 : 0;
+#else
     on = 0;  // fused pre-phase compiled out (QS_FUSED_PACK=0 in linear_tc.cu)
+#endif
   }
   return on == 1;
 }
