@@ -407,12 +407,17 @@ def main() -> None:
                                  "ms_per_ar_step": round(r["ms"] / r["steps"], 3)}
     e2e = run_e2e(model, a, a.batch, prompts)
     # reference cost model (costmodel.py:237-257) fed with a MEASURED latency profile
-    from paper_2410_11305_b200.costmodel import AcceptanceModel, analytic_speedup, measure_profile
+    from paper_2410_11305_b200.costmodel import (AcceptanceModel, analytic_speedup, geometric_acceptance,
+                                                 measure_profile)
     prof = measure_profile(model, [a.batch], ns=(1, 2, a.gamma + 1), ctx=a.prompt + a.new // 4)
     pred = analytic_speedup(prof, AcceptanceModel.from_trace(main_q["accept_lens"], a.gamma), a.gamma, a.batch)
+    # what other draft lengths would give on the same kernels (i.i.d. per-draft acceptance = measured rate)
+    by_gamma = {str(gm): round(analytic_speedup(prof, geometric_acceptance(main_q["acceptance_rate"], gm), gm,
+                                                a.batch).speedup, 3) for gm in (1, 2, 3, 4)}
     cost_model = {"profile_ms": {"draft": float(prof.draft[a.batch]),
                                  "verify": {str(n): round(float(c), 4) for n, c in prof.verify[a.batch]}},
-                  "predicted_speedup_vs_ar": round(pred.speedup, 4), "predicted_tokens_per_cycle":
+                  "predicted_speedup_vs_ar": round(pred.speedup, 4),
+                  "predicted_speedup_by_gamma_geometric": by_gamma, "predicted_tokens_per_cycle":
                   round(pred.tokens_per_cycle, 3), "acceptance_model": "empirical accept-length distribution of the timed run (device traces)"}
     roof = linear_roofline(model, a, main_q["profile"], a.batch, main_q["ctx_mean"])
     cpu = None
