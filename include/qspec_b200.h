@@ -44,7 +44,7 @@ enum { QS_MODE_HIGH = 0, QS_MODE_LOW = 1 }; /* quant.py:37-41 ExecutionMode */
 /* One quantised weight store in the device chunk layout. */
 typedef struct {
   const uint8_t* codes; /* [n_tiles][n_chunks][4][128][16] packed int4 */
-  const float* scales;  /* [G][n_pad] */
+  const float* scales;  /* [n_tiles][n_chunks][128], tile-major */
   int32_t n, k, g, n_pad, n_tiles, G, gp, cpg, n_chunks;
 } qs_qweight_t;
 

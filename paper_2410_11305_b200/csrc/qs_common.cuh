@@ -8,7 +8,8 @@
 //          (two's-complement nibbles, k relative to the chunk).  Groups of g
 //          codes are zero-padded to gp = roundup(g, 128) so every chunk belongs
 //          to exactly one quantisation group (cpg = gp/128 chunks per group).
-//   scales [G][n_pad] fp32 (group-major so a tile reads one coalesced row).
+//   scales [n_tiles][n_chunks][128] fp32 (tile-major: one stage of a tile reads one
+//          contiguous run; a group of gp > 128 repeats its scale in each of its chunks).
 // Activation operand image (produced per step by act_pack):
 //   img    [n_chunks][r_pad][128] int8, 128B-swizzled K-major (UMMA SW128),
 //          row = token*L + limb.  L = 1 (W4A4 draft: int4 codes in int8),
