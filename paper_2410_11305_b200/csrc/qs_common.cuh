@@ -14,7 +14,7 @@
 //   img    [n_chunks][r_pad][128] int8, 128B-swizzled K-major (UMMA SW128),
 //          row = token*L + limb.  L = 1 (W4A4 draft: int4 codes in int8),
 //          L = 3 (W4A16 verify: 24-bit fixed point split in three int8 limbs).
-//   ascale [G][a_ld] fp32 per (group, token): s_x (draft) or 2^-e (verify).
+//   ascale [n_chunks][a_ld] fp32 per (chunk, token): s_x (draft) or 2^-e (verify).
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>

@@ -70,6 +70,9 @@ def test_fcfs_matches_standalone(mode):
             Q.generate_greedy(model, r.prompt, Q.ExecutionMode.HIGH_PRECISION, c)
         assert out[r.id].new_tokens == ref.new_tokens, r.id
     assert stats.total_new_tokens == sum(len(v.new_tokens) for v in out.values())
+    # per-step cost units add up to the per-request totals (serving.py:182-187)
+    assert sum(stats.step_draft_units) == pytest.approx(stats.draft_cost_units)
+    assert sum(stats.step_verify_units) == pytest.approx(stats.verify_cost_units)
 
 
 @pytest.mark.gpu
