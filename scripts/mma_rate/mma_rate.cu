@@ -1,0 +1,137 @@
+// Microbenchmark (research tool, not part of the product library): issue rate of
+// tcgen05.mma.kind::i8 with A in TMEM, 1-SM (M=128) vs 2-SM pair (M=256), vs N.
+// Data is zero; only the time per instruction matters.
+#include <cstdint>
+#include <cstdio>
+#include <cuda_runtime.h>
+#include "../../paper_2410_11305_b200/csrc/ptx.cuh"
+
+using namespace qs;
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+template <int N, int CG, int ST>
+__global__ void __launch_bounds__(256, 1) mma_rate_kernel(int reps, unsigned long long* out, int* stop) {
+  extern __shared__ __align__(1024) uint8_t sm_raw[];
+  uint8_t* sm = sm_raw + ((1024u - (smem_u32(sm_raw) & 1023u)) & 1023u);
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tslot;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  constexpr int kBRows = CG == 2 ? N / 2 : N;  // each CTA of a pair holds half of B
+  for (int i = tid; i < kBRows * 128 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = 0;
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+  }
+  if (warp == 0) {
+    if (CG == 2) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tslot)));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      tmem_alloc<512>(&tslot);
+    }
+  }
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  if (CG == 2) cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = tslot;
+  const bool leader = CG == 1 || cluster_rank() == 0;
+  if (ST && warp >= 4 && warp < 8) {  // concurrent A staging traffic: tcgen05.st 32x32b.x32 into cols [128, 256)
+    const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+    uint32_t v[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = i;
+    volatile int* vs = stop;
+    const unsigned long long ts0 = gtimer();
+    int n = 0;
+    while (*vs == 0 && gtimer() - ts0 < 2000000000ull) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_st32(tmem + lane_base + 128 + c * 32, v);
+      tmem_wait_st();
+      ++n;
+    }
+    if ((tid & 31) == 0) out[148 + blockIdx.x * 4 + (warp & 3)] = n;
+  }
+  if (warp == 0 && leader) {
+    const uint64_t bdesc = sdesc_sw128(smem_u32(sm));
+    const uint32_t idesc = idesc_i8(CG == 2 ? 256 : 128, N);
+    const unsigned long long t0 = gtimer();
+    for (int r = 0; r < reps; ++r) {
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        if (CG == 2) {
+          asm volatile(
+              "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+              "@e tcgen05.mma.cta_group::2.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem),
+              "r"(tmem + 256 + kk * 8), "l"(bdesc + (uint64_t)(kk * 2)), "r"(idesc), "r"(kk)
+              : "memory");
+        } else {
+          mma_i8_ts_elect(tmem, tmem + 256 + kk * 8, bdesc + (uint64_t)(kk * 2), idesc, kk);
+        }
+      }
+    }
+    if (CG == 2) {
+      asm volatile(
+          "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+          "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(&bar))
+          : "memory");
+    } else {
+      mma_commit_elect(&bar);
+    }
+    mbar_wait(&bar, 0);
+    const unsigned long long t1 = gtimer();
+    if (tid == 0) {
+      out[blockIdx.x] = t1 - t0;
+      *reinterpret_cast<volatile int*>(stop) = 1;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (CG == 2) cluster_sync();
+  if (warp == 0) {
+    tc_fence_after();
+    if (CG == 2)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+    else
+      tmem_dealloc<512>(tmem);
+  }
+}
+
+template <int N, int CG, int ST>
+static int run(int reps, unsigned long long* out, int grid, int* stop) {
+  const size_t smem = (CG == 2 ? N / 2 : N) * 128 + 2048;
+  cudaFuncSetAttribute(mma_rate_kernel<N, CG, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CG;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, mma_rate_kernel<N, CG, ST>, reps, out, stop);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  return e == cudaSuccess ? 0 : (int)e;
+}
+
+extern "C" int mma_rate(int n, int cg, int reps, unsigned long long* out, int grid, int st, int* stop) {
+#define CASE(NN)                                                                        \
+  if (n == NN) {                                                                        \
+    if (st) return cg == 2 ? run<NN, 2, 1>(reps, out, grid, stop) : run<NN, 1, 1>(reps, out, grid, stop); \
+    return cg == 2 ? run<NN, 2, 0>(reps, out, grid, stop) : run<NN, 1, 0>(reps, out, grid, stop); \
+  }
+  CASE(8) CASE(16) CASE(32) CASE(64) CASE(128) CASE(192) CASE(256)
+  return -1;
+}
