@@ -279,14 +279,10 @@ __global__ void __launch_bounds__(512, 1) linear_tc_kernel(const LinearArgs a) {
         const uint32_t d0 = tmem + b * CPS * C::kAccCols;
         const uint32_t a0 = tmem + C::kAColBase + as_ * CPS * 32;
 #pragma unroll
-        for (int q = 0; q < CPS; ++q) {
-          if (q < it.nq) {
-#pragma unroll
-            for (int kk = 0; kk < 4; ++kk)
-              mma_i8_ts_elect(d0 + q * C::kAccCols, a0 + q * 32 + kk * 8,
-                              bdesc0 + (uint64_t)((q * C::kActBytes + kk * 32) >> 4), idesc, kk);
-          }
-        }
+        for (int q = 0; q < CPS; ++q)
+          if (q < it.nq)
+            mma_i8_ts_chunk4_elect(d0 + q * C::kAccCols, a0 + q * 32,
+                                   bdesc0 + (uint64_t)((q * C::kActBytes) >> 4), idesc);
         if (dbg0 && i < 64 && lane == 0) a.dbg[8 * 64 + i] = gtimer();
         mma_commit_elect(&empty[s]);
         mma_commit_elect(&tempty[as_]);

@@ -203,6 +203,26 @@ __device__ __forceinline__ void mbar_arrive_expect_tx_elect(uint64_t* bar, uint3
       : "memory");
 }
 
+// The four K-steps (32 bytes each) of one 128-wide chunk in one asm block, executed
+// by the whole (converged) warp with one elected lane issuing: A advances 8 TMEM
+// columns and the SW128 B descriptor 32 bytes (2 x 16 B units) per step; the first
+// step overwrites D, the rest accumulate.  One elect per chunk instead of per MMA.
+__device__ __forceinline__ void mma_i8_ts_chunk4_elect(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
+                                                       uint32_t idesc) {
+  asm volatile(
+      "{\n\t.reg .pred p0, p1, e;\n\t.reg .b32 a1, a2, a3;\n\t.reg .b64 b1, b2, b3;\n\t"
+      "setp.ne.b32 p0, %0, %0;\n\tsetp.eq.b32 p1, %0, %0;\n\t"
+      "add.u32 a1, %1, 8;\n\tadd.u32 a2, %1, 16;\n\tadd.u32 a3, %1, 24;\n\t"
+      "add.u64 b1, %2, 2;\n\tadd.u64 b2, %2, 4;\n\tadd.u64 b3, %2, 6;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [a1], b1, %3, p1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [a2], b2, %3, p1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [a3], b3, %3, p1;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc)
+      : "memory");
+}
+
 // Same, A from shared memory (used by the self-test of the descriptor path).
 __device__ __forceinline__ void mma_i8_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
                                           uint32_t accumulate) {
