@@ -8,6 +8,8 @@
 
 using namespace qs;
 
+__device__ const uint8_t* g_src;
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -45,7 +47,27 @@ __global__ void __launch_bounds__(256, 1) mma_rate_kernel(int reps, unsigned lon
   tc_fence_after();
   const uint32_t tmem = tslot;
   const bool leader = CG == 1 || cluster_rank() == 0;
-  if (ST && warp >= 4 && warp < 8) {  // concurrent A staging traffic: tcgen05.st 32x32b.x32 into cols [128, 256)
+  if (ST == 2 && warp == 4) {  // concurrent TMA traffic: 32 KB bulk copies global -> smem, back to back
+    __shared__ uint64_t cbar;
+    uint8_t* dst = sm + 64 * 1024;
+    if (lane_id() == 0) {
+      mbar_init(&cbar, 1);
+      fence_mbar_init();
+      volatile int* vs = stop;
+      uint32_t ph = 0;
+      int n = 0;
+      const unsigned long long ts0 = gtimer();
+      while (*vs == 0 && gtimer() - ts0 < 2000000000ull) {
+        mbar_arrive_expect_tx(&cbar, 32768);
+        bulk_g2s(dst, g_src + (size_t)((blockIdx.x * 7 + n) % 64) * 32768, 32768, &cbar);
+        mbar_wait(&cbar, ph);
+        ph ^= 1;
+        ++n;
+      }
+      out[148 + blockIdx.x * 4] = n;
+    }
+  }
+  if (ST == 1 && warp >= 4 && warp < 8) {  // concurrent A staging traffic: tcgen05.st 32x32b.x32 into cols [128, 256)
     const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
     uint32_t v[32];
 #pragma unroll
@@ -108,7 +130,7 @@ __global__ void __launch_bounds__(256, 1) mma_rate_kernel(int reps, unsigned lon
 
 template <int N, int CG, int ST>
 static int run(int reps, unsigned long long* out, int grid, int* stop) {
-  const size_t smem = (CG == 2 ? N / 2 : N) * 128 + 2048;
+  const size_t smem = 64 * 1024 + 32 * 1024 + 2048;
   cudaFuncSetAttribute(mma_rate_kernel<N, CG, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
@@ -126,9 +148,12 @@ static int run(int reps, unsigned long long* out, int grid, int* stop) {
   return e == cudaSuccess ? 0 : (int)e;
 }
 
+extern "C" int mma_set_src(const void* p) { return cudaMemcpyToSymbol(g_src, &p, sizeof(p)) == cudaSuccess ? 0 : 1; }
+
 extern "C" int mma_rate(int n, int cg, int reps, unsigned long long* out, int grid, int st, int* stop) {
 #define CASE(NN)                                                                        \
   if (n == NN) {                                                                        \
+    if (st == 2) return run<NN, 1, 2>(reps, out, grid, stop);                               \
     if (st) return cg == 2 ? run<NN, 2, 1>(reps, out, grid, stop) : run<NN, 1, 1>(reps, out, grid, stop); \
     return cg == 2 ? run<NN, 2, 0>(reps, out, grid, stop) : run<NN, 1, 0>(reps, out, grid, stop); \
   }

@@ -9,9 +9,12 @@ lib = C.CDLL(os.path.join(os.path.dirname(os.path.abspath(__file__)), "libmma_ra
 lib.mma_rate.argtypes = [C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_void_p]
 out = torch.zeros(148 + 148 * 4, dtype=torch.int64, device="cuda")
 stop = torch.zeros(1, dtype=torch.int32, device="cuda")
+src = torch.zeros(64 * 32768, dtype=torch.uint8, device="cuda")
+lib.mma_set_src.argtypes = [C.c_void_p]
+lib.mma_set_src(src.data_ptr())
 reps = 2000
 for st, cg, n in [(0, 1, 8), (0, 1, 16), (0, 1, 32), (0, 1, 64), (0, 1, 128), (0, 1, 192), (0, 1, 256),
-                  (0, 2, 32), (0, 2, 64), (0, 2, 192), (1, 1, 8), (1, 1, 16), (1, 1, 192)]:
+                  (0, 2, 32), (0, 2, 64), (0, 2, 192), (1, 1, 8), (1, 1, 16), (1, 1, 192), (2, 1, 8), (2, 1, 16)]:
     if True:
         grid = 148
         out.zero_(); stop.zero_()
@@ -25,7 +28,10 @@ for st, cg, n in [(0, 1, 8), (0, 1, 16), (0, 1, 32), (0, 1, 64), (0, 1, 128), (0
         ns = float(v.mean()) / (reps * 4)
         rows_per_sm = 128  # per SM: M=256 pair covers 128 rows on each SM
         extra = ""
-        if st:
+        if st == 2:
+            nb = allv[148:148 + 148 * 4].reshape(148, 4)[:, 0]
+            extra = f"; concurrent bulk copies: {nb[nb > 0].mean() * 32768 / float(v.mean()):.1f} B/ns per SM"
+        elif st:
             sts = allv[148:148 + 148 * 4].reshape(148, 4)
             iters = sts[sts > 0].mean()
             t_ns = float(v.mean())
