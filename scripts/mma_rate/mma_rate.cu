@@ -128,6 +128,86 @@ __global__ void __launch_bounds__(256, 1) mma_rate_kernel(int reps, unsigned lon
   }
 }
 
+// ST=3: the kernel's A staging pattern: 4 warps tcgen05.st a 32-column A slot (ring of 2),
+// wait::st + fence + mbarrier arrive; the MMA warp waits, issues 4 MMAs on that slot,
+// commits to the slot's "empty" barrier.  Time per slot (4 MMAs) vs the free-running rate.
+template <int N, int SL, int CH>
+__global__ void __launch_bounds__(256, 1) turnaround_kernel(int reps, unsigned long long* out) {
+  extern __shared__ __align__(1024) uint8_t sm_raw[];
+  uint8_t* sm = sm_raw + ((1024u - (smem_u32(sm_raw) & 1023u)) & 1023u);
+  __shared__ uint64_t full[SL], empty[SL];
+  __shared__ uint32_t tslot;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int i = tid; i < N * 128 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = 0;
+  if (tid == 0) {
+    for (int i = 0; i < SL; ++i) { mbar_init(&full[i], 4); mbar_init(&empty[i], 1); }
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc<512>(&tslot);
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tslot;
+  if (warp == 0) {
+    const uint64_t bdesc = sdesc_sw128(smem_u32(sm));
+    const uint32_t idesc = idesc_i8(128, N);
+    const unsigned long long t0 = gtimer();
+    for (int r = 0; r < reps; ++r) {
+      const int b = r % SL;
+      mbar_wait(&full[b], (r / SL) & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int c = 0; c < CH; ++c)
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          mma_i8_ts_elect(tmem + c * 8, tmem + 128 + (b * CH + c) * 32 + kk * 8, bdesc + (uint64_t)(kk * 2), idesc, kk);
+      mma_commit_elect(&empty[b]);
+    }
+    mbar_wait(&empty[(reps - 1) % SL], ((reps - 1) / SL) & 1);
+    const unsigned long long t1 = gtimer();
+    if (tid == 0) out[blockIdx.x] = t1 - t0;
+  } else if (warp >= 4) {
+    const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+    uint32_t v[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = i * lane;
+    for (int r = 0; r < reps; ++r) {
+      const int b = r % SL;
+      if (r >= SL) mbar_wait(&empty[b], ((r / SL) & 1) ^ 1);
+      tc_fence_after();
+#pragma unroll
+      for (int c = 0; c < CH; ++c) tmem_st32(tmem + lane_base + 128 + (b * CH + c) * 32, v);
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&full[b]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc<512>(tmem);
+  }
+}
+
+template <int SL, int CH>
+static int turn(int reps, unsigned long long* out) {
+  const size_t smem = 64 * 1024;
+  cudaFuncSetAttribute(turnaround_kernel<8, SL, CH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  turnaround_kernel<8, SL, CH><<<148, 256, smem>>>(reps, out);
+  return cudaDeviceSynchronize() == cudaSuccess ? 0 : 1;
+}
+extern "C" int mma_turnaround(int slots, int chunks, int reps, unsigned long long* out) {
+  if (slots == 2 && chunks == 1) return turn<2, 1>(reps, out);
+  if (slots == 4 && chunks == 1) return turn<4, 1>(reps, out);
+  if (slots == 8 && chunks == 1) return turn<8, 1>(reps, out);
+  if (slots == 2 && chunks == 4) return turn<2, 4>(reps, out);
+  if (slots == 3 && chunks == 4) return turn<3, 4>(reps, out);
+  return -1;
+}
+
 template <int N, int CG, int ST>
 static int run(int reps, unsigned long long* out, int grid, int* stop) {
   const size_t smem = 64 * 1024 + 32 * 1024 + 2048;

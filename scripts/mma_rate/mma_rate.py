@@ -38,3 +38,13 @@ for st, cg, n in [(0, 1, 8), (0, 1, 16), (0, 1, 32), (0, 1, 64), (0, 1, 128), (0
             extra = f"; concurrent tcgen05.st: {iters * 4 * 4096 * 4 / t_ns:.1f} B/ns per SM (4 warps)"
         print(f"st={st} cg={cg} M={128 * cg} N={n:3d}: {ns:6.1f} ns per MMA instruction; "
               f"{rows_per_sm * 32 / ns:6.1f} int8 A bytes/ns per SM{extra}", flush=True)
+
+lib.mma_turnaround.argtypes = [C.c_int, C.c_int, C.c_int, C.c_void_p]
+for sl, ch in ((2, 1), (4, 1), (8, 1), (2, 4), (3, 4)):
+    out.zero_()
+    rc = lib.mma_turnaround(sl, ch, reps, out.data_ptr())
+    v = out.cpu().numpy()[:148]
+    v = v[v > 0]
+    per = float(v.mean()) / reps
+    print(f"turnaround N=8 slots={sl} chunks/slot={ch}: {per:7.1f} ns per slot, {per / (4 * ch):5.1f} ns per MMA "
+          f"({8192 * ch / per:6.1f} packed-weight B/ns per SM); rc={rc}", flush=True)
