@@ -35,6 +35,9 @@
 #ifndef QS_FUSED_PACK
 #define QS_FUSED_PACK 0
 #endif
+#ifndef QS_CPS_SMALLN
+#define QS_CPS_SMALLN 4
+#endif
 
 namespace qs {
 
@@ -43,7 +46,9 @@ struct LinCfg {
   static constexpr int kRowsMax = (L * TMAX) <= 8 ? 8 : ((L * TMAX + 15) / 16) * 16;
   static constexpr int kAccCols = kRowsMax;  // one accumulator block (N columns) per chunk
   // chunks per stage: as many as TMEM allows with 2 acc buffers + 2 A slots
-  static constexpr int kCPS = (2 * 4 * kAccCols + 2 * 4 * 32 <= 512) ? 4
+  // (QS_CPS_SMALLN=6 builds 6-chunk stages where TMEM allows: measured neutral)
+  static constexpr int kCPS = (QS_CPS_SMALLN == 6 && 2 * 6 * kAccCols + 2 * 6 * 32 <= 512) ? 6
+                              : (2 * 4 * kAccCols + 2 * 4 * 32 <= 512) ? 4
                               : (2 * 2 * kAccCols + 2 * 2 * 32 <= 512) ? 2 : 1;
   // spend leftover TMEM on deeper rings (lets unpack / epilogue run further ahead)
   static constexpr int kFree0 = 512 - 2 * kCPS * kAccCols - 2 * kCPS * 32;
@@ -55,11 +60,6 @@ struct LinCfg {
   static_assert(kAColBase + kASlots * kCPS * 32 <= kTmemCols, "TMEM budget");
   static constexpr int kActBytes = kRowsMax * 128;
   static constexpr int kStageBytes = kCPS * (kChunkBytes + kActBytes);
-  static constexpr int kStages0 = (196 * 1024) / kStageBytes;
-  static constexpr int kStages = kStages0 > 8 ? 8 : kStages0;
-  static_assert(kStages >= 2, "pipeline depth");
-  static constexpr int kSStages = kStages + 2;
-  static constexpr int kSEntry = kCPS * (128 + (TMAX < 8 ? 8 : TMAX)) * 4;  // ascale rows are a_ld = roundup(T, 8)
   // 16 warps: 4 control, then unpack and epilogue warps (2 or 1 per TMEM lane
   // quadrant each).  Small T is unpack-bound -> 8 unpack warps; large T is
   // epilogue-bound -> 8 epilogue warps.
@@ -67,6 +67,18 @@ struct LinCfg {
   static constexpr int kEpiWarps = 12 - kUnpackWarps;
   static constexpr int kEpiHalves = kEpiWarps / 4;
   static constexpr int kUnpackHalves = kUnpackWarps / 4;
+  static constexpr int kStages0 = (196 * 1024) / kStageBytes;
+  // Unpack group g takes the stages i with i % kUnpackHalves == g and waits on
+  // wfull[i % kStages] by parity.  kStages must be a multiple of kUnpackHalves so
+  // that each weight slot is only ever consumed by ONE group, which then observes
+  // every phase of that slot's barrier; otherwise a group that skipped a phase can
+  // read a parity two phases stale and unpack a slot whose bulk copy is in flight.
+  static constexpr int kStagesCap = kStages0 > 8 ? 8 : kStages0;
+  static constexpr int kStages = kStagesCap - kStagesCap % kUnpackHalves;
+  static_assert(kStages >= 2, "pipeline depth");
+  static_assert(kStages % kUnpackHalves == 0, "unpack groups must own whole weight slots");
+  static constexpr int kSStages = kStages + 2;
+  static constexpr int kSEntry = kCPS * (128 + (TMAX < 8 ? 8 : TMAX)) * 4;  // ascale rows are a_ld = roundup(T, 8)
   static constexpr int kEpiThreads = kEpiWarps * 32;
   static constexpr int kTokChunk = TMAX < 8 ? TMAX : 8;  // tokens per epilogue token chunk (T <= 4 buckets: fewer)
   static constexpr int kOwnChunks = ((TMAX < 8 ? 8 : TMAX) / 8 + kEpiHalves - 1) / kEpiHalves;  // per epilogue warp
@@ -307,9 +319,10 @@ __global__ void __launch_bounds__(512, 1) linear_tc_kernel(const LinearArgs a) {
       tc_fence_after();
       if (dbg0 && i < 64 && r == 0) a.dbg[9 * 64 + i] = gtimer();
       // all LDS of the stage first (latency overlap), then unpack + TMEM stores
+      constexpr int kPre = CPS <= 4 ? CPS : 1;  // register budget
       uint4 wv[CPS][4];
 #pragma unroll
-      for (int q = 0; q < CPS; ++q) {
+      for (int q = 0; q < kPre; ++q) {
         if (q < it.nq) {
           const uint4* src = reinterpret_cast<const uint4*>(smem + s * C::kStageBytes + q * kChunkBytes);
 #pragma unroll
@@ -319,6 +332,11 @@ __global__ void __launch_bounds__(512, 1) linear_tc_kernel(const LinearArgs a) {
 #pragma unroll
       for (int q = 0; q < CPS; ++q) {
         if (q < it.nq) {
+          if (q >= kPre) {
+            const uint4* src = reinterpret_cast<const uint4*>(smem + s * C::kStageBytes + q * kChunkBytes);
+#pragma unroll
+            for (int jp = 0; jp < 4; ++jp) wv[q][jp] = src[jp * 128 + r];
+          }
           uint32_t v[32];
 #pragma unroll
           for (int jp = 0; jp < 4; ++jp) {
