@@ -113,22 +113,27 @@ __device__ __forceinline__ float token_inv_rms(const PackArgs& a, int t, int tid
 }
 
 // One warp quantises group gi of token t into the operand image (+ scales).
-template <int L>
+// kPlain: the common operand (no attention combine, g % 4 == 0, gp == 128) -- one
+// float4 per lane and none of the general paths, so the kernel's code stays small
+// (the general instantiation is ~12k instructions; instruction fetch dominated it).
+template <int L, bool kPlain = false>
 __device__ __forceinline__ void pack_group(const PackArgs& a, int t, int gi, float inv, int lane) {
   const int K = a.K;
   const float* src_row = a.gather_ids != nullptr ? a.emb + (size_t)a.gather_ids[t] * K : a.x + (size_t)t * a.ldx;
-  const int g = a.g, cpg = a.gp >> 7;
-  constexpr int kMaxIter = 4;  // gp <= 512
+  const int g = a.g, cpg = kPlain ? 1 : a.gp >> 7;
+  constexpr int kMaxIter = kPlain ? 1 : 4;  // gp <= 512
   float val[kMaxIter][4];
   float m = 0.f;
-  const bool vec = (a.att_o == nullptr) && ((g & 3) == 0);
-  const bool att4 = (a.att_o != nullptr) && ((g & 3) == 0) && ((a.att_hd & 3) == 0);
+  const bool vec = kPlain || ((a.att_o == nullptr) && ((g & 3) == 0));
+  const bool att4 = !kPlain && (a.att_o != nullptr) && ((g & 3) == 0) && ((a.att_hd & 3) == 0);
 #pragma unroll
   for (int it = 0; it < kMaxIter; ++it) {
     const int o0 = it * 128 + lane * 4;
     float4 raw = make_float4(0.f, 0.f, 0.f, 0.f);
     if (vec && o0 < g) raw = *reinterpret_cast<const float4*>(src_row + gi * g + o0);
-    if (att4 && o0 < g) raw = merge4(a, t, gi * g + o0);
+    if constexpr (!kPlain) {
+      if (att4 && o0 < g) raw = merge4(a, t, gi * g + o0);
+    }
     const float rv[4] = {raw.x, raw.y, raw.z, raw.w};
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
@@ -136,7 +141,11 @@ __device__ __forceinline__ void pack_group(const PackArgs& a, int t, int gi, flo
       float v = 0.f;
       if (o < g) {
         const int k = gi * g + o;
-        v = (vec || att4) ? rv[e] : pack_load(a, t, k, src_row);
+        if constexpr (kPlain) {
+          v = rv[e];
+        } else {
+          v = (vec || att4) ? rv[e] : pack_load(a, t, k, src_row);
+        }
         if (a.x_out) a.x_out[(size_t)t * K + k] = v;
         if (a.rms_w != nullptr) v = __fmul_rn(__fmul_rn(v, inv), a.rms_w[k]);
         if (a.y_out) a.y_out[(size_t)t * K + k] = v;
@@ -173,7 +182,7 @@ __device__ __forceinline__ void pack_group(const PackArgs& a, int t, int gi, flo
 #pragma unroll
   for (int it = 0; it < kMaxIter; ++it) {
     const int o = it * 128 + lane * 4;
-    if (it * 128 >= a.gp) break;
+    if (!kPlain && it * 128 >= a.gp) break;
     uint32_t w[L];
 #pragma unroll
     for (int l = 0; l < L; ++l) w[l] = 0;
