@@ -126,7 +126,18 @@ struct StageIt {
   }
 };
 
-template <int L, int TMAX>
+// Post-op class fixed at compile time so a launch only carries its own epilogue
+// tail (the tail runs once per CTA with a cold instruction cache): OPC = kOpStore
+// covers store / residual / dump (runtime a.op), every other class is exact.
+template <int OPC, int O>
+__device__ __forceinline__ bool op_is(const LinearArgs& a) {
+  constexpr bool in_class = OPC == kOpStore ? (O == kOpStore || O == kOpResidual || O == kOpDump) : O == OPC;
+  if constexpr (!in_class) return false;
+  if constexpr (OPC != kOpStore) return true;
+  return a.op == O;
+}
+
+template <int L, int TMAX, int OPC>
 __global__ void __launch_bounds__(512, 1) linear_tc_kernel(const LinearArgs a) {
   using C = LinCfg<L, TMAX>;
   constexpr int CPS = C::kCPS;
@@ -380,7 +391,7 @@ __global__ void __launch_bounds__(512, 1) linear_tc_kernel(const LinearArgs a) {
       if (dbg0 && i < 64 && et == 0) a.dbg[10 * 64 + i] = gtimer();
       const float* se = sring + ss * (C::kSEntry / 4);
       bool released = false;  // accumulator buffer b handed back to the MMA
-      if (a.op == kOpDump) {
+      if (op_is<OPC, kOpDump>(a)) {
         if (h == 0) {
           for (int q = 0; q < it.nq; ++q) {
             const uint32_t col0 = tmem + lane_base + (b * CPS + q) * C::kAccCols;
@@ -464,7 +475,7 @@ __global__ void __launch_bounds__(512, 1) linear_tc_kernel(const LinearArgs a) {
       // ---- segment end (stages never straddle tiles): stream-K fixup + post-op
       const int last_u = tile * NC + it.ch0 + it.nq - 1;
       const bool seg_end = (it.ch0 + it.nq == NC) || (last_u == u1 - 1);
-      if (!seg_end || a.op == kOpDump) continue;
+      if (!seg_end || op_is<OPC, kOpDump>(a)) continue;
       if (a.dbg && et == 0) a.dbg[3584 + c] = gtimer();
       const int c_lo = cta_of_unit(tile * NC, U, P);
       const int c_hi = cta_of_unit(tile * NC + NC - 1, U, P);
@@ -523,16 +534,16 @@ __global__ void __launch_bounds__(512, 1) linear_tc_kernel(const LinearArgs a) {
         for (int e = 0; e < 8; ++e) {
           const int t = (kH * lc + h) * 8 + e;
           const float v = acc[lc * 8 + e];
-          if (a.op == kOpStore || a.op == kOpResidual) {
+          if (op_is<OPC, kOpStore>(a) || op_is<OPC, kOpResidual>(a)) {
             if (t < a.T && valid) {
               float* o = a.out + (size_t)t * a.ldo + n;
-              *o = (a.op == kOpResidual) ? __fadd_rn(*o, v) : v;
+              *o = (op_is<OPC, kOpResidual>(a)) ? __fadd_rn(*o, v) : v;
             }
-          } else if (a.op == kOpSiluMul) {
+          } else if (op_is<OPC, kOpSiluMul>(a)) {
             const float other = __shfl_xor_sync(0xffffffffu, v, 1);
             if (t < a.T && valid && (r & 1) == 0)
               a.out[(size_t)t * a.ldo + (n >> 1)] = __fmul_rn(silu_ref(v), other);
-          } else if (a.op == kOpQkvRope) {
+          } else if (op_is<OPC, kOpQkvRope>(a)) {
             const float other = __shfl_xor_sync(0xffffffffu, v, 1);
             if (t < a.T && valid) {
               const bool is_v = n >= a.n_q + a.n_k;
@@ -557,7 +568,7 @@ __global__ void __launch_bounds__(512, 1) linear_tc_kernel(const LinearArgs a) {
                 (is_v ? a.vcache : a.kcache)[off] = val;
               }
             }
-          } else if (a.op == kOpLogits) {
+          } else if (op_is<OPC, kOpLogits>(a)) {
             if (t < a.T) {
               if (a.out != nullptr && valid) a.out[(size_t)t * a.ldo + n] = v;
               float bv = valid ? v : -INFINITY;
@@ -573,7 +584,7 @@ __global__ void __launch_bounds__(512, 1) linear_tc_kernel(const LinearArgs a) {
           }
         }
       }
-      if (a.op == kOpLogits) {
+      if (op_is<OPC, kOpLogits>(a)) {
         named_bar(1, kEpiT);
         if (et < a.T) {
           float bv = red_val[et];
@@ -625,18 +636,28 @@ __global__ void __launch_bounds__(512, 1) linear_tc_kernel(const LinearArgs a) {
   if (a.dbg && threadIdx.x == 0) a.dbg[2048 + c] = gtimer();
 }
 
-template <int L, int TMAX>
-static cudaError_t launch_linear_t(const LinearArgs& a, cudaStream_t st) {
+template <int L, int TMAX, int OPC>
+static cudaError_t launch_linear_op(const LinearArgs& a, cudaStream_t st) {
   using C = LinCfg<L, TMAX>;
-  if (a.r_pad != C::kRowsMax) return cudaErrorInvalidValue;  // image rows are padded to the bucket
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(linear_tc_kernel<L, TMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(linear_tc_kernel<L, TMAX, OPC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          C::kSmemBytes);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  return launch_k(linear_tc_kernel<L, TMAX>, dim3(a.n_cta), dim3(512), C::kSmemBytes, st, a);
+  return launch_k(linear_tc_kernel<L, TMAX, OPC>, dim3(a.n_cta), dim3(512), C::kSmemBytes, st, a);
+}
+
+template <int L, int TMAX>
+static cudaError_t launch_linear_t(const LinearArgs& a, cudaStream_t st) {
+  if (a.r_pad != LinCfg<L, TMAX>::kRowsMax) return cudaErrorInvalidValue;  // image rows are padded to the bucket
+  switch (a.op) {
+    case kOpSiluMul: return launch_linear_op<L, TMAX, kOpSiluMul>(a, st);
+    case kOpQkvRope: return launch_linear_op<L, TMAX, kOpQkvRope>(a, st);
+    case kOpLogits: return launch_linear_op<L, TMAX, kOpLogits>(a, st);
+    default: return launch_linear_op<L, TMAX, kOpStore>(a, st);
+  }
 }
 
 // token buckets; the 3-limb (verify / AR) path adds T <= 2 and T <= 4 (6 / 12 image
