@@ -35,6 +35,12 @@
 #ifndef QS_FUSED_PACK
 #define QS_FUSED_PACK 0
 #endif
+// per-stage globaltimer stamps for scripts/linear_timeline.py (build with
+// QS_NVCC_EXTRA=-DQS_LIN_TIMELINE=1); compiled out by default: the checks sit in
+// the MMA issuer's loop
+#ifndef QS_LIN_TIMELINE
+#define QS_LIN_TIMELINE 0
+#endif
 #ifndef QS_CPS_SMALLN
 #define QS_CPS_SMALLN 4
 #endif
@@ -166,8 +172,8 @@ __global__ void __launch_bounds__(512, 1) linear_tc_kernel(const LinearArgs a) {
   const int NC = a.n_chunks;
   const int U = a.n_tiles * NC, P = a.n_cta, c = blockIdx.x;
   const int u0 = unit_bound(c, U, P), u1 = unit_bound(c + 1, U, P);
-  const bool dbg0 = a.dbg != nullptr && c == 0;
-  if (a.dbg && threadIdx.x == 0) a.dbg[1024 + c] = gtimer();
+  const bool dbg0 = QS_LIN_TIMELINE && a.dbg != nullptr && c == 0;
+  if (QS_LIN_TIMELINE && a.dbg && threadIdx.x == 0) a.dbg[1024 + c] = gtimer();
   pdl_launch_dependents();
 
   if (threadIdx.x == 0) {
@@ -325,7 +331,7 @@ __global__ void __launch_bounds__(512, 1) linear_tc_kernel(const LinearArgs a) {
       if ((i % C::kUnpackHalves) != ug) continue;
       const int s = i % C::kStages, b = i % C::kASlots;
       mbar_wait_warp(&wfull[s], (i / C::kStages) & 1, 0);
-      if (a.dbg && i == 0 && r == 0) a.dbg[3072 + c] = gtimer();
+      if (QS_LIN_TIMELINE && a.dbg && i == 0 && r == 0) a.dbg[3072 + c] = gtimer();
       mbar_wait_warp(&tempty[b], ((i / C::kASlots) & 1) ^ 1, 0);
       tc_fence_after();
       if (dbg0 && i < 64 && r == 0) a.dbg[9 * 64 + i] = gtimer();
@@ -476,7 +482,7 @@ __global__ void __launch_bounds__(512, 1) linear_tc_kernel(const LinearArgs a) {
       const int last_u = tile * NC + it.ch0 + it.nq - 1;
       const bool seg_end = (it.ch0 + it.nq == NC) || (last_u == u1 - 1);
       if (!seg_end || op_is<OPC, kOpDump>(a)) continue;
-      if (a.dbg && et == 0) a.dbg[3584 + c] = gtimer();
+      if (QS_LIN_TIMELINE && a.dbg && et == 0) a.dbg[3584 + c] = gtimer();
       const int c_lo = cta_of_unit(tile * NC, U, P);
       const int c_hi = cta_of_unit(tile * NC + NC - 1, U, P);
       if (c_hi > c_lo) {
@@ -633,7 +639,7 @@ __global__ void __launch_bounds__(512, 1) linear_tc_kernel(const LinearArgs a) {
     tc_fence_after();
     tmem_dealloc<C::kTmemCols>(tmem);
   }
-  if (a.dbg && threadIdx.x == 0) a.dbg[2048 + c] = gtimer();
+  if (QS_LIN_TIMELINE && a.dbg && threadIdx.x == 0) a.dbg[2048 + c] = gtimer();
 }
 
 template <int L, int TMAX, int OPC>

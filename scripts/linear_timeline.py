@@ -1,6 +1,8 @@
 """%globaltimer timeline of one tensor-core linear launch (pipeline diagnosis).
 
 Per-CTA entry / exit times for all CTAs and per-stage role events for CTA 0.
+The stamps are compiled out by default: build with
+QS_NVCC_EXTRA=-DQS_LIN_TIMELINE=1 python -c "from paper_2410_11305_b200 import build as b; b.build(force=True)"
 """
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
