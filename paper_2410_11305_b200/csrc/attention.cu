@@ -91,10 +91,17 @@ __global__ void __launch_bounds__(256) attn_partial_kernel(const AttnArgs a) {
   float* vt = kt + kAttnChunk * hd;           // [chunk][hd]
   float* sc = vt + kAttnChunk * hd;           // [Q][chunk]
   __shared__ int ctx_s[64];
+  __shared__ long long row_s[kAttnChunk];  // element offset of each key row of the chunk
 
   const int sl = a.slot[tok0];
   const int* bt = a.block_table + (size_t)sl * a.bt_ld;
   if (tid < Q) ctx_s[tid] = a.pos[tok0 + tid / hpk] + 1;
+  // page-table walk once per key row (not once per 16-byte copy)
+  for (int jj = tid; jj < nk; jj += blockDim.x) {
+    const int j = j0 + jj;
+    row_s[jj] = (((long long)bt[j / a.page] * a.KV + kvh) * a.page + (j % a.page)) * hd;
+  }
+  __syncthreads();
   // async loads: queries, then the chunk's K and V rows (16 B per op)
   const int hd4 = hd >> 2;
   for (int e = tid; e < Q * hd4; e += blockDim.x) {
@@ -103,8 +110,8 @@ __global__ void __launch_bounds__(256) attn_partial_kernel(const AttnArgs a) {
     cp_async16(qv + qi * hd + d4 * 4, a.q + (size_t)(tok0 + i) * a.ldq + (size_t)h * hd + d4 * 4);
   }
   for (int e = tid; e < nk * hd4; e += blockDim.x) {
-    const int jj = e / hd4, d4 = e - jj * hd4, j = j0 + jj;
-    const size_t row = (((size_t)bt[j / a.page] * a.KV + kvh) * a.page + (j % a.page)) * hd + d4 * 4;
+    const int jj = e / hd4, d4 = e - jj * hd4;
+    const size_t row = (size_t)row_s[jj] + d4 * 4;
     cp_async16(kt + jj * hd + d4 * 4, a.kcache + row);
     cp_async16(vt + jj * hd + d4 * 4, a.vcache + row);
   }
