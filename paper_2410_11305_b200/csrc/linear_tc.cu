@@ -38,6 +38,10 @@
 // per-stage globaltimer stamps for scripts/linear_timeline.py (build with
 // QS_NVCC_EXTRA=-DQS_LIN_TIMELINE=1); compiled out by default: the checks sit in
 // the MMA issuer's loop
+// largest token bucket that gets 8 unpack warps (and 4 epilogue warps)
+#ifndef QS_UNPACK8_TMAX
+#define QS_UNPACK8_TMAX 8
+#endif
 #ifndef QS_LIN_TIMELINE
 #define QS_LIN_TIMELINE 0
 #endif
@@ -69,7 +73,7 @@ struct LinCfg {
   // 16 warps: 4 control, then unpack and epilogue warps (2 or 1 per TMEM lane
   // quadrant each).  Small T is unpack-bound -> 8 unpack warps; large T is
   // epilogue-bound -> 8 epilogue warps.
-  static constexpr int kUnpackWarps = TMAX <= 8 ? 8 : 4;
+  static constexpr int kUnpackWarps = TMAX <= QS_UNPACK8_TMAX ? 8 : 4;
   static constexpr int kEpiWarps = 12 - kUnpackWarps;
   static constexpr int kEpiHalves = kEpiWarps / 4;
   static constexpr int kUnpackHalves = kUnpackWarps / 4;
