@@ -19,7 +19,7 @@ namespace qs {
 constexpr int kGroupsPerCta = 4;
 constexpr int kPackThreads = 32 * kGroupsPerCta;
 
-template <int L, bool kPlain>
+template <int L, bool kPlain, bool kAttPlain>
 __global__ void __launch_bounds__(kPackThreads) act_pack_kernel(const PackArgs a) {
   __shared__ float red[kGroupsPerCta];
   pdl_launch_dependents();
@@ -29,19 +29,23 @@ __global__ void __launch_bounds__(kPackThreads) act_pack_kernel(const PackArgs a
   if (a.rms_w != nullptr) inv = token_inv_rms(a, t, tid, kPackThreads, 1, red);
   const int gi = blockIdx.y * kGroupsPerCta + warp;
   if (gi >= a.G) return;
-  pack_group<L, kPlain>(a, t, gi, inv, lane);
+  pack_group<L, kPlain, kAttPlain>(a, t, gi, inv, lane);
 }
 
 cudaError_t launch_act_pack(int L, const PackArgs& a, cudaStream_t st) {
   if (a.gp > 512) return cudaErrorInvalidValue;
   const dim3 grid(a.T, (a.G + kGroupsPerCta - 1) / kGroupsPerCta);
-  const bool plain = a.att_o == nullptr && (a.g & 3) == 0 && a.gp == 128 && a.g <= 128;
-  if (plain) {
-    if (L == 1) return launch_k(act_pack_kernel<1, true>, grid, dim3(kPackThreads), 0, st, a);
-    return launch_k(act_pack_kernel<3, true>, grid, dim3(kPackThreads), 0, st, a);
+  const bool lean = (a.g & 3) == 0 && a.gp == 128 && a.g <= 128;
+  if (lean && a.att_o == nullptr) {
+    if (L == 1) return launch_k(act_pack_kernel<1, true, false>, grid, dim3(kPackThreads), 0, st, a);
+    return launch_k(act_pack_kernel<3, true, false>, grid, dim3(kPackThreads), 0, st, a);
   }
-  if (L == 1) return launch_k(act_pack_kernel<1, false>, grid, dim3(kPackThreads), 0, st, a);
-  return launch_k(act_pack_kernel<3, false>, grid, dim3(kPackThreads), 0, st, a);
+  if (lean && (a.att_hd & 3) == 0) {
+    if (L == 1) return launch_k(act_pack_kernel<1, false, true>, grid, dim3(kPackThreads), 0, st, a);
+    return launch_k(act_pack_kernel<3, false, true>, grid, dim3(kPackThreads), 0, st, a);
+  }
+  if (L == 1) return launch_k(act_pack_kernel<1, false, false>, grid, dim3(kPackThreads), 0, st, a);
+  return launch_k(act_pack_kernel<3, false, false>, grid, dim3(kPackThreads), 0, st, a);
 }
 
 }  // namespace qs

@@ -116,16 +116,18 @@ __device__ __forceinline__ float token_inv_rms(const PackArgs& a, int t, int tid
 // kPlain: the common operand (no attention combine, g % 4 == 0, gp == 128) -- one
 // float4 per lane and none of the general paths, so the kernel's code stays small
 // (the general instantiation is ~12k instructions; instruction fetch dominated it).
-template <int L, bool kPlain = false>
+// kAttPlain: the same for the attention-combine operand (att_hd % 4 == 0).
+template <int L, bool kPlain = false, bool kAttPlain = false>
 __device__ __forceinline__ void pack_group(const PackArgs& a, int t, int gi, float inv, int lane) {
+  constexpr bool kLean = kPlain || kAttPlain;
   const int K = a.K;
   const float* src_row = a.gather_ids != nullptr ? a.emb + (size_t)a.gather_ids[t] * K : a.x + (size_t)t * a.ldx;
-  const int g = a.g, cpg = kPlain ? 1 : a.gp >> 7;
-  constexpr int kMaxIter = kPlain ? 1 : 4;  // gp <= 512
+  const int g = a.g, cpg = kLean ? 1 : a.gp >> 7;
+  constexpr int kMaxIter = kLean ? 1 : 4;  // gp <= 512
   float val[kMaxIter][4];
   float m = 0.f;
-  const bool vec = kPlain || ((a.att_o == nullptr) && ((g & 3) == 0));
-  const bool att4 = !kPlain && (a.att_o != nullptr) && ((g & 3) == 0) && ((a.att_hd & 3) == 0);
+  const bool vec = kPlain || (!kAttPlain && (a.att_o == nullptr) && ((g & 3) == 0));
+  const bool att4 = kAttPlain || (!kPlain && (a.att_o != nullptr) && ((g & 3) == 0) && ((a.att_hd & 3) == 0));
 #pragma unroll
   for (int it = 0; it < kMaxIter; ++it) {
     const int o0 = it * 128 + lane * 4;
@@ -141,7 +143,7 @@ __device__ __forceinline__ void pack_group(const PackArgs& a, int t, int gi, flo
       float v = 0.f;
       if (o < g) {
         const int k = gi * g + o;
-        if constexpr (kPlain) {
+        if constexpr (kLean) {
           v = rv[e];
         } else {
           v = (vec || att4) ? rv[e] : pack_load(a, t, k, src_row);
@@ -182,7 +184,7 @@ __device__ __forceinline__ void pack_group(const PackArgs& a, int t, int gi, flo
 #pragma unroll
   for (int it = 0; it < kMaxIter; ++it) {
     const int o = it * 128 + lane * 4;
-    if (!kPlain && it * 128 >= a.gp) break;
+    if (!kLean && it * 128 >= a.gp) break;
     uint32_t w[L];
 #pragma unroll
     for (int l = 0; l < L; ++l) w[l] = 0;
