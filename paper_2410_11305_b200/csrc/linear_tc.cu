@@ -48,6 +48,9 @@
 #ifndef QS_CPS_SMALLN
 #define QS_CPS_SMALLN 4
 #endif
+#ifndef QS_ONE_ACC
+#define QS_ONE_ACC 0
+#endif
 
 namespace qs {
 
@@ -57,14 +60,20 @@ struct LinCfg {
   static constexpr int kAccCols = kRowsMax;  // one accumulator block (N columns) per chunk
   // chunks per stage: as many as TMEM allows with 2 acc buffers + 2 A slots
   // (QS_CPS_SMALLN=6 builds 6-chunk stages where TMEM allows: measured neutral)
-  static constexpr int kCPS = (QS_CPS_SMALLN == 6 && 2 * 6 * kAccCols + 2 * 6 * 32 <= 512) ? 6
-                              : (2 * 4 * kAccCols + 2 * 4 * 32 <= 512) ? 4
-                              : (2 * 2 * kAccCols + 2 * 2 * 32 <= 512) ? 2 : 1;
+  static constexpr int kCPS0 = (QS_CPS_SMALLN == 6 && 2 * 6 * kAccCols + 2 * 6 * 32 <= 512) ? 6
+                               : (2 * 4 * kAccCols + 2 * 4 * 32 <= 512) ? 4
+                               : (2 * 2 * kAccCols + 2 * 2 * 32 <= 512) ? 2 : 1;
+  // wide buckets (N = 192): ONE accumulator buffer of 2-chunk stages instead of two of
+  // 1-chunk stages -- half the unpack -> MMA hand-offs per weight byte; the epilogue
+  // hands the buffer back right after its tcgen05.ld
+  static constexpr bool kOneAcc = QS_ONE_ACC && kCPS0 == 1 && (2 * kAccCols + 2 * 2 * 32 <= 512);
+  static constexpr int kCPS = kOneAcc ? 2 : kCPS0;
   // spend leftover TMEM on deeper rings (lets unpack / epilogue run further ahead)
-  static constexpr int kFree0 = 512 - 2 * kCPS * kAccCols - 2 * kCPS * 32;
+  static constexpr int kFree0 = 512 - (kOneAcc ? 1 : 2) * kCPS * kAccCols - 2 * kCPS * 32;
   static constexpr int kASlots = 2 + (kFree0 >= kCPS * 32 ? 1 : 0);
   static constexpr int kFree1 = kFree0 - (kASlots - 2) * kCPS * 32;
-  static constexpr int kAccBufs = 2 + (kFree1 / (kCPS * kAccCols) > 2 ? 2 : kFree1 / (kCPS * kAccCols));
+  static constexpr int kAccBufs =
+      kOneAcc ? 1 : 2 + (kFree1 / (kCPS * kAccCols) > 2 ? 2 : kFree1 / (kCPS * kAccCols));
   static constexpr int kAColBase = kAccBufs * kCPS * kAccCols;
   static constexpr int kTmemCols = 512;
   static_assert(kAColBase + kASlots * kCPS * 32 <= kTmemCols, "TMEM budget");
