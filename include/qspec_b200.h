@@ -13,9 +13,9 @@
  *   qs_repack_ref                        <- storage.py:352-422 load_checkpoint (codes+scales)
  *   qs_act_quant                         <- quant.py:179-194 _quantize_groups,
  *                                           quant.py:229-245 fake_quantize_activations
+ *   qs_rmsnorm                           <- numerics.py:46-62 rmsnorm (numpy pairwise sum order)
  *   qs_w4a4_linear / qs_w4a16_linear     <- quant.py:248-261 qlinear_forward (LOW / HIGH)
  *   qs_forward                           <- model.py:255-348 forward
- *   qs_forward_mk                        <- model.py:255-348 forward (one persistent launch)
  *   qs_forward_tp                        <- model.py:255-348 forward, one tensor-parallel shard
  *   qs_draft_prep / qs_verify_prep /
  *   qs_accept / qs_ar_prep / qs_ar_commit <- specdec.py:103-176, 258-335 (+ model.py:211-229 kv_commit)
@@ -135,6 +135,9 @@ int qs_repack_ref(const uint8_t* ref_codes, const float* ref_scales, int32_t row
 /* ------------------------------------------------------------- operators */
 int qs_act_quant(const float* x, int32_t T, int32_t K, int32_t g, int8_t* codes, float* scales, float* fq,
                  void* stream);
+/* numerics.py:46-62 rmsnorm: y = (x * (1/sqrt(mean(x^2) + eps))) * w per row, bit-exact
+ * with numpy (pairwise float32 sum of squares); x, y [T, K] fp32 device, w [K]. */
+int qs_rmsnorm(const float* x, const float* w, int32_t T, int32_t K, float eps, float* y, void* stream);
 int qs_w4a4_linear(const qs_qweight_t* w, const float* x, int32_t T, float* y, const qs_workspace_t* ws,
                    void* stream);
 int qs_w4a16_linear(const qs_qweight_t* w, const float* x, int32_t T, float* y, const qs_workspace_t* ws,
@@ -154,17 +157,19 @@ int qs_linear_group_dots(const qs_qweight_t* w, const float* x, int32_t T, int32
  * records become event nodes when qs_forward is captured into a CUDA graph. */
 int qs_profile_enable(int32_t max_launches); /* 0 disables */
 int qs_profile_reset(void);
+/* Device timeline of every forward-path launch enqueued while enabled: buf is a device
+ * array of cap pairs (start, end) the caller fills with (UINT64_MAX, 0); each launch
+ * takes the next pair and folds %globaltimer of every CTA's entry (min) and exit (max)
+ * into it -- also when replayed from a CUDA graph captured while enabled.  Tags as for
+ * qs_profile_read (mode*16 + kind, kind 5 = operand pack, 6 = attention).  buf NULL
+ * disables; qs_ktrace_read returns the tags in launch order. */
+int qs_ktrace_enable(uint64_t* buf, int32_t cap);
+int qs_ktrace_read(int32_t* tags, int32_t max_out, int32_t* n_out);
 int qs_profile_read(float* ms, int32_t* tags, int32_t max_out, int32_t* n_out);
 
 /* ------------------------------------------------------------------ step */
 int qs_forward(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const qs_workspace_t* ws, float* logits,
                int32_t* argmax, void* stream);
-/* Same forward, same results bit for bit, as ONE persistent kernel (forward_mk.cu):
- * weights stream continuously while device counters order the phases.  The
- * first call for a given (model, batch, workspace, mode) builds and uploads the
- * phase program (synchronous); later calls -- and graph captures -- only launch. */
-int qs_forward_mk(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const qs_workspace_t* ws, float* logits,
-                  int32_t* argmax, void* stream);
 
 /* Tensor-parallel forward (config 3, 13B TP 2/4/8): the model struct holds ONE
  * rank's shard -- q/k/v and gate/up column-split (n_heads, n_kv_heads, d_ff are

@@ -239,6 +239,36 @@ def rmsnorm(x: np.ndarray, w: np.ndarray, eps: float) -> np.ndarray:
     return x * (F32(1.0) / np.sqrt(ms + F32(eps))) * w
 
 
+def pairwise_sum_f32(v: np.ndarray) -> np.float32:
+    """numpy's float32 add-reduce order along a contiguous row (the ``pairwise_sum`` of
+    numpy/_core/src/umath/loops_utils.h.src), which ``np.mean(x * x, dtype=float32)`` in
+    numerics.py:60 runs: n < 8 sequential from 0; n <= 128 eight strided accumulators in
+    order, ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), then the n % 8 tail; else split at
+    n/2 - (n/2) % 8.  Explicit restatement of the order the device RMSNorm implements
+    (``csrc/pack_dev.cuh`` token_inv_rms); ``rmsnorm`` above uses numpy itself."""
+    v = np.asarray(v, dtype=np.float32)
+    n = v.shape[0]
+    if n < 8:
+        r = F32(0.0)
+        for x in v:
+            r = F32(r + x)
+        return r
+    if n <= 128:
+        r = [v[j] for j in range(8)]
+        i = 8
+        while i < n - n % 8:
+            for j in range(8):
+                r[j] = F32(r[j] + v[i + j])
+            i += 8
+        res = F32(F32(F32(r[0] + r[1]) + F32(r[2] + r[3])) + F32(F32(r[4] + r[5]) + F32(r[6] + r[7])))
+        for k in range(i, n):
+            res = F32(res + v[k])
+        return res
+    n2 = n // 2
+    n2 -= n2 % 8
+    return F32(pairwise_sum_f32(v[:n2]) + pairwise_sum_f32(v[n2:]))
+
+
 def softmax(s: np.ndarray) -> np.ndarray:
     e = np.exp(s - np.max(s, axis=-1, keepdims=True))
     return e / np.sum(e, axis=-1, keepdims=True, dtype=np.float32)

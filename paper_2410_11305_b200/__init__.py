@@ -10,6 +10,7 @@ from .errors import (CheckpointError, ConfigError, QSpecError, SequenceOverflowE
                      TraceError, WorkloadError)
 from .model import (CostCounter, KVCache, LayerWeights, LogitsBlock, ModelConfig, TransformerModel, WriteTarget,
                     forward, kv_commit, kv_memory_report, kv_reset)
+from .numerics import rmsnorm
 from .quant import (ExecutionMode, QuantizedTensor, activation_quant_calls, dequantize,
                     fake_quantize_activations, pack_int4, qlinear_forward, quantize_groupwise,
                     reset_activation_quant_calls, start_qlinear_log, stop_qlinear_log, unpack_int4)

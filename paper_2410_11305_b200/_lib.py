@@ -77,6 +77,9 @@ _SIGS = {
     "qs_quantize_weight": ([vp, i32, i32, i32, vp, vp, i32, i32, i32, vp, vp, vp], C.c_int),
     "qs_lcg_fill": ([vp, u64, u64, i64, f32, vp], C.c_int),
     "qs_repack_ref": ([vp, vp, i32, i32, i32, vp, vp, i32, i32, i32, vp], C.c_int),
+    "qs_ktrace_enable": ([vp, i32], C.c_int),
+    "qs_ktrace_read": ([vp, i32, C.POINTER(i32)], C.c_int),
+    "qs_rmsnorm": ([vp, vp, i32, i32, f32, vp, vp], C.c_int),
     "qs_act_quant": ([vp, i32, i32, i32, vp, vp, vp, vp], C.c_int),
     "qs_w4a4_linear": ([C.POINTER(QWeight), vp, i32, vp, C.POINTER(Workspace), vp], C.c_int),
     "qs_w4a16_linear": ([C.POINTER(QWeight), vp, i32, vp, C.POINTER(Workspace), vp], C.c_int),
@@ -87,7 +90,6 @@ _SIGS = {
     "qs_profile_reset": ([], C.c_int),
     "qs_profile_read": ([vp, vp, i32, C.POINTER(i32)], C.c_int),
     "qs_forward": ([C.POINTER(Model), C.POINTER(Batch), i32, C.POINTER(Workspace), vp, vp, vp], C.c_int),
-    "qs_forward_mk": ([C.POINTER(Model), C.POINTER(Batch), i32, C.POINTER(Workspace), vp, vp, vp], C.c_int),
     "qs_forward_tp": ([C.POINTER(Model), C.POINTER(Batch), i32, C.POINTER(Workspace), vp, vp, i32, vp, vp, vp],
                       C.c_int),
     "qs_draft_prep": ([C.POINTER(Seq), i32, vp], C.c_int),

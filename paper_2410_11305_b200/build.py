@@ -36,6 +36,12 @@ def _stale(out: str, deps: list[str]) -> bool:
 
 def build(verbose: bool = False, force: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
+    extra = os.environ.get("QS_NVCC_EXTRA", "").split()
+    # objects built with other flags (e.g. an experiment knob in QS_NVCC_EXTRA) are stale
+    stamp = os.path.join(BUILD, "flags.stamp")
+    flags = " ".join([NVCC, *ARCH, *FLAGS, *extra])
+    if not os.path.exists(stamp) or open(stamp).read() != flags:
+        force = True
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
     headers.append(os.path.join(HERE, "..", "include", "qspec_b200.h"))
     objs, jobs = [], []
@@ -43,7 +49,6 @@ def build(verbose: bool = False, force: bool = False) -> str:
         obj = os.path.join(BUILD, os.path.basename(src)[:-3] + ".o")
         objs.append(obj)
         if force or _stale(obj, [src] + headers):
-            extra = os.environ.get("QS_NVCC_EXTRA", "").split()
             jobs.append([NVCC, *ARCH, *FLAGS, *extra, "-c", src, "-o", obj])
 
     def run(cmd: list[str]) -> None:
@@ -59,6 +64,8 @@ def build(verbose: bool = False, force: bool = False) -> str:
         list(ex.map(run, jobs))
     if force or jobs or _stale(LIB, objs):
         run([NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart"])
+    with open(stamp, "w") as f:
+        f.write(flags)
     return LIB
 
 

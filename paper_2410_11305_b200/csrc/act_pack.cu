@@ -11,7 +11,8 @@
 //
 // Grid: (token, block of kGroupsPerCta groups), 32 threads per group.  A CTA
 // that needs RMSNorm re-reads the whole row for the sum of squares (L2-resident,
-// fixed reduction order, so every CTA of a token computes the same scale).
+// numpy's pairwise order, so every CTA of a token computes the reference's scale
+// bit for bit).
 #include "pack_dev.cuh"
 
 namespace qs {
@@ -21,7 +22,8 @@ constexpr int kPackThreads = 32 * kGroupsPerCta;
 
 template <int L, bool kPlain, bool kAttPlain>
 __global__ void __launch_bounds__(kPackThreads) act_pack_kernel(const PackArgs a) {
-  __shared__ float red[kGroupsPerCta];
+  __shared__ float red[132];
+  KTraceScope kts(a.kt);
   pdl_launch_dependents();
   pdl_wait();
   const int t = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;

@@ -74,6 +74,7 @@ __device__ __forceinline__ void score_block(const float* kt, const float* qv, fl
 
 __global__ void __launch_bounds__(256) attn_partial_kernel(const AttnArgs a) {
   extern __shared__ __align__(16) float sm[];
+  KTraceScope kts(a.kt);
   pdl_launch_dependents();
   pdl_wait();
   const int blk = blockIdx.x, kvh = blockIdx.y, ch = blockIdx.z, tid = threadIdx.x;
@@ -194,11 +195,14 @@ int attention_chunk_len() { return kAttnChunk; }
 
 cudaError_t launch_attention(const AttnArgs& a, int n_blk, cudaStream_t st) {
   const size_t smem = attention_smem_bytes(a.qmax, a.hpk, a.hd, a.ctx_cap);
-  static size_t attr = 0;
-  if (smem > 48 * 1024 && smem > attr) {
-    cudaError_t e = cudaFuncSetAttribute(attn_partial_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  static size_t attr[kMaxDevices] = {};  // the attribute is per device
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (smem > 48 * 1024 && (dev >= kMaxDevices || smem > attr[dev])) {
+    e = cudaFuncSetAttribute(attn_partial_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    attr = smem;
+    if (dev < kMaxDevices) attr[dev] = smem;
   }
   return launch_k(attn_partial_kernel, dim3(n_blk, a.KV, attention_chunks(a.ctx_cap)), dim3(256), smem, st, a);
 }

@@ -30,11 +30,6 @@
 // so an n-token call is bit-identical to n single-token calls.
 #include "pack_dev.cuh"
 
-// The fused operand-pack pre-phase (grid barrier inside the linear) is kept for
-// experiments; the default path packs in a separate PDL-overlapped launch.
-#ifndef QS_FUSED_PACK
-#define QS_FUSED_PACK 0
-#endif
 // per-stage globaltimer stamps for scripts/linear_timeline.py (build with
 // QS_NVCC_EXTRA=-DQS_LIN_TIMELINE=1); compiled out by default: the checks sit in
 // the MMA issuer's loop
@@ -53,6 +48,8 @@
 #endif
 
 namespace qs {
+
+constexpr size_t kPfPiece = 64 * 1024;  // bytes per cp.async.bulk.prefetch.L2
 
 template <int L, int TMAX>
 struct LinCfg {
@@ -177,9 +174,6 @@ __global__ void __launch_bounds__(512, 1) linear_tc_kernel(const LinearArgs a) {
   int* flag = reinterpret_cast<int*>(tmem_slot + 2);
   float* red_val = reinterpret_cast<float*>(tmem_slot + 4);  // [4][TMAX]
   int* red_idx = reinterpret_cast<int*>(red_val + 4 * TMAX);  // [4][TMAX]
-  volatile int* gen0_s = reinterpret_cast<volatile int*>(red_idx + 4 * TMAX);  // grid-barrier generation at entry
-  float* pk_red = reinterpret_cast<float*>(red_idx + 4 * TMAX + 4);            // [12] rms partials
-  float* pk_inv = pk_red + 16;                                                 // [4] per-token 1/rms
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int NC = a.n_chunks;
@@ -187,6 +181,7 @@ __global__ void __launch_bounds__(512, 1) linear_tc_kernel(const LinearArgs a) {
   const int u0 = unit_bound(c, U, P), u1 = unit_bound(c + 1, U, P);
   const bool dbg0 = QS_LIN_TIMELINE && a.dbg != nullptr && c == 0;
   if (QS_LIN_TIMELINE && a.dbg && threadIdx.x == 0) a.dbg[1024 + c] = gtimer();
+  ktrace_enter(a.kt);
   pdl_launch_dependents();
 
   if (threadIdx.x == 0) {
@@ -205,7 +200,6 @@ __global__ void __launch_bounds__(512, 1) linear_tc_kernel(const LinearArgs a) {
     }
     for (int i = 0; i < C::kSStages; ++i) { mbar_init(&sfull[i], 1); mbar_init(&sempty[i], C::kEpiWarps); }
     fence_mbar_init();
-    *gen0_s = -1;
   }
   if (warp == 2) tmem_alloc<C::kTmemCols>(tmem_slot);
   tc_fence_before();
@@ -213,42 +207,6 @@ __global__ void __launch_bounds__(512, 1) linear_tc_kernel(const LinearArgs a) {
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const uint32_t act_bytes = (uint32_t)a.r_pad * 128u;
-
-  // ---------------------------------------------------------------- fused pack pre-phase
-  // Warps 4..15 quantise this CTA's share of the (token, group) operand items into
-  // the global image while warp 0 is already streaming weights; a grid barrier
-  // (all CTAs are co-resident: grid <= #SMs, 1 CTA/SM) publishes the image before
-  // any activation copy is issued.
-#if QS_FUSED_PACK
-  if (a.fuse_pack && warp >= 4) {
-    pdl_wait();
-    const int ptid = threadIdx.x - 128;
-    if (ptid == 0) *gen0_s = ld_acquire(&a.gbar[1]);
-    const PackArgs& pk = a.pk;
-    const int TG = pk.T * pk.G;
-    const int p0 = (int)umul_div(c, TG, P), p1 = (int)umul_div(c + 1, TG, P);
-    if (p0 < p1) {
-      const int t_first = p0 / pk.G, t_last = (p1 - 1) / pk.G;
-      for (int tt = t_first; tt <= t_last; ++tt) {  // token by token: 1/rms, then its groups
-        float inv = 1.0f;
-        if (pk.rms_w != nullptr) {
-          inv = token_inv_rms(pk, tt, ptid, 384, 2, pk_red);
-        }
-        const int q0 = max(p0, tt * pk.G), q1 = min(p1, (tt + 1) * pk.G);
-        for (int p = q0 + (warp - 4); p < q1; p += 12) pack_group<L>(pk, tt, p - tt * pk.G, inv, lane);
-      }
-    }
-    fence_proxy_async_global();  // generic-proxy image writes -> later bulk (async-proxy) reads
-    named_bar(2, 384);
-    if (ptid == 0) {
-      const int old = atom_add_acq_rel(&a.gbar[0], 1);
-      if (old == P - 1) {
-        a.gbar[0] = 0;
-        red_release_add(&a.gbar[1], 1);
-      }
-    }
-  }
-#endif
 
   if (warp == 0) {
     // ------------------------------------------------------------ weight/act producer (warp-wide, elected issue)
@@ -264,8 +222,37 @@ __global__ void __launch_bounds__(512, 1) linear_tc_kernel(const LinearArgs a) {
         bulk_g2s_elect(st, a.codes + ((size_t)it.tile * NC + it.ch0) * kChunkBytes, it.nq * kChunkBytes,
                        &wfull[npro]);
       }
+      // L2 prefetch (no smem, no barrier): the rest of this CTA's own weight range, then
+      // its share of the forward's look-ahead window (later linears' weights)
+      if (lane == 0) {
+        if (a.pf_own) {
+          const size_t b0 = ((size_t)it.u) * kChunkBytes, b1 = (size_t)u1 * kChunkBytes;
+          for (size_t o = b0; o < b1; o += kPfPiece)
+            prefetch_l2(a.codes + o, (uint32_t)(b1 - o < kPfPiece ? b1 - o : kPfPiece));
+          const size_t s0 = (size_t)u0 * kTileN * 4, s1 = (size_t)u1 * kTileN * 4;
+          if (s1 > s0) prefetch_l2(reinterpret_cast<const uint8_t*>(a.wscale) + s0, (uint32_t)(s1 - s0));
+        }
+        if (a.pf_n > 0) {
+          size_t tot = 0;
+          for (int r = 0; r < a.pf_n; ++r) tot += a.pf_len[r];
+          // CTA c takes [c*tot/P, (c+1)*tot/P) of the concatenated ranges, 16-byte aligned
+          size_t lo = (tot * (size_t)c / P) & ~(size_t)15, hi = (tot * (size_t)(c + 1) / P) & ~(size_t)15;
+          if (c == P - 1) hi = tot;
+          size_t base = 0;
+          for (int r = 0; r < a.pf_n && lo < hi; ++r) {
+            const size_t e = base + a.pf_len[r];
+            if (lo < e) {
+              const size_t x0 = lo - base, x1 = (hi < e ? hi : e) - base;
+              for (size_t o = x0; o < x1; o += kPfPiece)
+                prefetch_l2(a.pf_ptr[r] + o, (uint32_t)(x1 - o < kPfPiece ? x1 - o : kPfPiece));
+              lo = base + x1;
+            }
+            base = e;
+          }
+        }
+      }
+      __syncwarp();
       pdl_wait();
-      if (QS_FUSED_PACK && a.fuse_pack) grid_barrier_wait(gen0_s, a.gbar);
       StageIt ia{u0, u1, NC, CPS};
       for (int i = 0; i < npro && ia.next(); ++i) {
         uint8_t* st = smem + i * C::kStageBytes;
@@ -288,7 +275,6 @@ __global__ void __launch_bounds__(512, 1) linear_tc_kernel(const LinearArgs a) {
     // ------------------------------------------------------------ scale producer (warp-wide, elected issue)
     {
       pdl_wait();
-      if (QS_FUSED_PACK && a.fuse_pack) grid_barrier_wait(gen0_s, a.gbar);
       const uint32_t a_bytes = (uint32_t)a.a_ld * 4u;
       StageIt it{u0, u1, NC, CPS};
       for (int i = 0; it.next(); ++i) {
@@ -519,7 +505,11 @@ __global__ void __launch_bounds__(512, 1) linear_tc_kernel(const LinearArgs a) {
           continue;
         }
         if (et == 0) {
+          // same 5 s trap guard as the mbarrier waits: a missing contributor (CTAs not
+          // co-resident) fails the launch instead of wedging the GPU
+          const unsigned long long t0 = gtimer();
           while (ld_acquire(&a.counters[tile]) != c_hi - c_lo) {
+            if (gtimer() - t0 > 5000000000ull) __trap();
           }
           a.counters[tile] = 0;
         }
@@ -653,17 +643,21 @@ __global__ void __launch_bounds__(512, 1) linear_tc_kernel(const LinearArgs a) {
     tmem_dealloc<C::kTmemCols>(tmem);
   }
   if (QS_LIN_TIMELINE && a.dbg && threadIdx.x == 0) a.dbg[2048 + c] = gtimer();
+  ktrace_exit(a.kt);
 }
 
 template <int L, int TMAX, int OPC>
 static cudaError_t launch_linear_op(const LinearArgs& a, cudaStream_t st) {
   using C = LinCfg<L, TMAX>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(linear_tc_kernel<L, TMAX, OPC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         C::kSmemBytes);
+  static bool attr[kMaxDevices] = {};  // the attribute is per device
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev >= kMaxDevices || !attr[dev]) {
+    e = cudaFuncSetAttribute(linear_tc_kernel<L, TMAX, OPC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             C::kSmemBytes);
     if (e != cudaSuccess) return e;
-    attr = true;
+    if (dev < kMaxDevices) attr[dev] = true;
   }
   return launch_k(linear_tc_kernel<L, TMAX, OPC>, dim3(a.n_cta), dim3(512), C::kSmemBytes, st, a);
 }

@@ -77,38 +77,108 @@ __device__ __forceinline__ float4 merge4(const PackArgs& a, int t, int k) {
   return make_float4(__fdiv_rn(acc[0], Ls), __fdiv_rn(acc[1], Ls), __fdiv_rn(acc[2], Ls), __fdiv_rn(acc[3], Ls));
 }
 
-// 1/sqrt(mean(x^2) + eps) of token t's input row, computed cooperatively by
-// nthreads threads (fixed stride + fixed tree => identical in every CTA that
-// uses the same thread count).  bar_id/red: a named barrier and >= nthreads/32 floats.
+// numpy's pairwise float32 sum (numpy/_core/src/umath/loops_utils.h.src, pairwise_sum),
+// which np.mean(x * x, dtype=float32) uses along a contiguous row (numerics.py:60):
+//   n < 8     sequential from 0;
+//   n <= 128  8 strided accumulators r[j] = a[j] + a[8+j] + ... in order, then
+//             ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), then the n % 8 tail sequentially;
+//   n > 128   split at n2 = n/2 - (n/2)%8 and add the two halves' sums.
+// Serial restatement (one thread), for shapes whose recursion is not a balanced tree.
+static __device__ float pairwise_sumsq_serial(const float* x, int n) {
+  if (n < 8) {
+    float r = 0.f;
+    for (int i = 0; i < n; ++i) r = __fadd_rn(r, __fmul_rn(x[i], x[i]));
+    return r;
+  }
+  if (n <= 128) {
+    float r[8];
+    for (int j = 0; j < 8; ++j) r[j] = __fmul_rn(x[j], x[j]);
+    int i = 8;
+    for (; i < n - (n % 8); i += 8)
+      for (int j = 0; j < 8; ++j) r[j] = __fadd_rn(r[j], __fmul_rn(x[i + j], x[i + j]));
+    float res = __fadd_rn(__fadd_rn(__fadd_rn(r[0], r[1]), __fadd_rn(r[2], r[3])),
+                          __fadd_rn(__fadd_rn(r[4], r[5]), __fadd_rn(r[6], r[7])));
+    for (; i < n; ++i) res = __fadd_rn(res, __fmul_rn(x[i], x[i]));
+    return res;
+  }
+  int n2 = n / 2;
+  n2 -= n2 % 8;
+  return __fadd_rn(pairwise_sumsq_serial(x, n2), pairwise_sumsq_serial(x + n2, n - n2));
+}
+
+// 1/sqrt(mean(x^2) + eps) of token t's input row (numerics.py:46-62), bit-exact with
+// numpy: the row is cut into the pairwise recursion's leaves (n = Lf * 2^lev, Lf <= 128),
+// 8 lanes per leaf run its 8 accumulators in numpy's order and combine them with an xor
+// tree (= numpy's bracketing), and the leaf sums are combined by the balanced tree of the
+// recursion.  Unbalanced recursions (n/2 not a multiple of 8 somewhere) run serially.
+// nthreads (a multiple of 32) threads cooperate; red holds >= 130 floats; bar_id is a
+// named barrier for those threads.
 __device__ __forceinline__ float token_inv_rms(const PackArgs& a, int t, int tid, int nthreads, int bar_id,
                                                float* red) {
-  const float* src_row = a.gather_ids != nullptr ? a.emb + (size_t)a.gather_ids[t] * a.K : a.x + (size_t)t * a.ldx;
-  const float4* row4 = reinterpret_cast<const float4*>(src_row);
-  const int K4 = a.K >> 2;
-  float part = 0.f;
-  for (int base = 0; base < K4; base += 4 * nthreads) {
-    float4 v[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int k4 = base + u * nthreads + tid;
-      v[u] = k4 < K4 ? row4[k4] : make_float4(0.f, 0.f, 0.f, 0.f);
+  const float* row = a.gather_ids != nullptr ? a.emb + (size_t)a.gather_ids[t] * a.K : a.x + (size_t)t * a.ldx;
+  const int n = a.K;
+  int Lf = n, lev = 0;
+  bool bal = true;
+  while (Lf > 128) {
+    int h = Lf >> 1;
+    h -= h % 8;
+    if (2 * h != Lf || lev >= 7) {
+      bal = false;
+      break;
     }
+    Lf = h;
+    ++lev;
+  }
+  float* total = red + 128;
+  if (!bal) {
+    if (tid == 0) *total = pairwise_sumsq_serial(row, n);
+  } else {
+    const int nl = 1 << lev, ngroups = nthreads >> 3, gi = tid >> 3, j = tid & 7;
+    for (int base = 0; base < nl; base += ngroups) {
+      const int b = base + gi;
+      const float* x = row + (size_t)(b < nl ? b : 0) * Lf;
+      float res = 0.f;
+      if (Lf < 8) {
+        for (int i = 0; i < Lf; ++i) res = __fadd_rn(res, __fmul_rn(x[i], x[i]));
+      } else {
+        const int m = Lf >> 3;  // <= 16 accumulator steps
+        float v[16];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      part = __fadd_rn(part, __fmul_rn(v[u].x, v[u].x));
-      part = __fadd_rn(part, __fmul_rn(v[u].y, v[u].y));
-      part = __fadd_rn(part, __fmul_rn(v[u].z, v[u].z));
-      part = __fadd_rn(part, __fmul_rn(v[u].w, v[u].w));
+        for (int i = 0; i < 16; ++i) v[i] = i < m ? x[8 * i + j] : 0.f;
+        float r = __fmul_rn(v[0], v[0]);
+#pragma unroll
+        for (int i = 1; i < 16; ++i)
+          if (i < m) r = __fadd_rn(r, __fmul_rn(v[i], v[i]));
+        r = __fadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 1));
+        r = __fadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 2));
+        r = __fadd_rn(r, __shfl_xor_sync(0xffffffffu, r, 4));
+        res = r;
+        for (int i = 8 * m; i < Lf; ++i) res = __fadd_rn(res, __fmul_rn(x[i], x[i]));
+      }
+      if (j == 0 && b < nl) red[b] = res;
+    }
+    named_bar(bar_id, nthreads);
+    if (tid < 32) {
+      // lane l holds the balanced sub-tree of leaves [l*per, (l+1)*per), then an xor tree
+      const int per = nl > 32 ? nl >> 5 : 1;
+      float s[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) s[i] = (i < per && tid * per + i < nl) ? red[tid * per + i] : 0.f;
+      if (per >= 2) s[0] = __fadd_rn(s[0], s[1]);
+      if (per >= 4) {
+        s[2] = __fadd_rn(s[2], s[3]);
+        s[0] = __fadd_rn(s[0], s[2]);
+      }
+      float v = s[0];
+      const int lanes = nl > 32 ? 32 : nl;
+      for (int off = 1; off < lanes; off <<= 1) v = __fadd_rn(v, __shfl_xor_sync(0xffffffffu, v, off));
+      if (tid == 0) *total = v;
     }
   }
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) part = __fadd_rn(part, __shfl_xor_sync(0xffffffffu, part, off));
-  if ((tid & 31) == 0) red[tid >> 5] = part;
   named_bar(bar_id, nthreads);
-  float ss = 0.f;
-  for (int w = 0; w < (nthreads >> 5); ++w) ss = __fadd_rn(ss, red[w]);
+  const float ss = *total;
   named_bar(bar_id, nthreads);  // red is reused by the next call
-  const float ms = __fdiv_rn(ss, (float)a.K);
+  const float ms = __fdiv_rn(ss, (float)n);
   return __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(ms, a.eps)));
 }
 

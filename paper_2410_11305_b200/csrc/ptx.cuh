@@ -284,23 +284,6 @@ __device__ __forceinline__ int atom_add_acq_rel(int* p, int v) {
 __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
-// Warp-wide wait for the kernel's grid barrier: generation must move past the
-// value sampled (into smem) by the pack threads before they arrived.
-__device__ __forceinline__ void grid_barrier_wait(volatile int* gen0_s, int* gbar) {
-  if ((threadIdx.x & 31) == 0) {
-    int g0;
-    const unsigned long long t0 = gtimer();
-    while ((g0 = *gen0_s) < 0) {
-      if (gtimer() - t0 > 5000000000ull) __trap();
-    }
-    while (ld_acquire(&gbar[1]) == g0) {
-      if (gtimer() - t0 > 5000000000ull) __trap();
-    }
-    fence_proxy_async_global();
-  }
-  __syncwarp();
-}
-
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));

@@ -42,6 +42,7 @@ inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
+constexpr int kMaxDevices = 64;  // per-device caches of kernel attributes
 constexpr int kTileN = 128;    // output rows per tile (UMMA M)
 constexpr int kChunkK = 128;   // K positions per chunk (one SW128 row of int8)
 constexpr int kChunkBytes = kTileN * kChunkK / 2;  // 8 KiB packed weights per (tile, chunk)
@@ -53,6 +54,31 @@ __host__ __device__ inline int img_rows(int T, int L) {
   int r = T * L;
   return r <= 8 ? 8 : round_up(r, 16);
 }
+
+// Per-launch device timeline (qs_ktrace_enable): thread 0 of every CTA folds its
+// %globaltimer at entry / exit into buf[2*slot] (min) / buf[2*slot+1] (max), so a
+// replayed CUDA graph yields each kernel's [first CTA start, last CTA end] without
+// breaking programmatic dependent launch.  buf == nullptr: off (one predicated branch).
+struct KTrace {
+  unsigned long long* buf;
+  int slot;
+};
+__device__ __forceinline__ unsigned long long kt_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void ktrace_enter(const KTrace& k) {
+  if (k.buf != nullptr && threadIdx.x == 0) atomicMin(&k.buf[2 * k.slot], kt_now());
+}
+__device__ __forceinline__ void ktrace_exit(const KTrace& k) {
+  if (k.buf != nullptr && threadIdx.x == 0) atomicMax(&k.buf[2 * k.slot + 1], kt_now());
+}
+struct KTraceScope {
+  const KTrace& k;
+  __device__ __forceinline__ explicit KTraceScope(const KTrace& k_) : k(k_) { ktrace_enter(k); }
+  __device__ __forceinline__ ~KTraceScope() { ktrace_exit(k); }
+};
 
 enum PostOp : int {
   kOpStore = 0,     // out[t, n] = y
@@ -83,7 +109,10 @@ struct PackArgs {
   const float* att_ml;  // [T][H][cmax][2]  (chunk max, chunk sum)
   const int* att_pos;   // [T] query positions (context = pos + 1)
   int att_hd, att_cmax, att_chunk;
+  KTrace kt;
 };
+
+constexpr int kMaxPf = 6;  // prefetch ranges per linear launch
 
 struct LinearArgs {
   const uint8_t* codes;
@@ -114,10 +143,18 @@ struct LinearArgs {
   int* argmax_out;
   // kOpDump
   int32_t* dump;
-  // fused operand pack pre-phase (replaces a separate act_pack launch)
+  // operand producer of this linear (run by a preceding act_pack launch)
   PackArgs pk;
-  int fuse_pack;
-  int* gbar;  // [2] grid barrier: arrival count, generation
+  // L2 prefetch.  Weights do not depend on activations, so HBM can stream ahead of the
+  // dependency chain: this launch prefetches the byte ranges pf_ptr/pf_len (pieces of
+  // LATER linears' codes and scales, a fixed window ahead in the forward's weight
+  // stream), split evenly over its CTAs; pf_own also prefetches this CTA's own units
+  // beyond what its shared-memory ring requests up front.
+  const uint8_t* pf_ptr[kMaxPf];
+  uint32_t pf_len[kMaxPf];
+  int pf_n;
+  int pf_own;
+  KTrace kt;
   // debug timeline (CTA 0): [role][i] globaltimer ns; roles: 0 producer issue, 1 unpack done,
   // 2 mma issued, 3 epilogue start (acc ready), 4 epilogue done
   unsigned long long* dbg;
@@ -144,26 +181,7 @@ struct AttnArgs {
   int qmax, ctx_cap;
   float* out;
   int ldo;
-};
-
-// Persistent forward kernel program (forward_mk.cu): one entry per phase.
-enum MkKind : int { kMkPack = 0, kMkLin = 1, kMkAttn = 2 };
-struct MkPhase {
-  int kind;
-  int dep;        // phase whose completion this phase waits for (-1: none)
-  int dep_count;  // completion count of that phase
-  int n_blk;      // kMkAttn: query blocks
-  LinearArgs lin;
-  PackArgs pk;
-  AttnArgs at;
-};
-struct MkArgs {
-  const MkPhase* prog;
-  int n_phases;
-  const int* lin_phase;  // phase index of each linear, in program order
-  int n_lin;
-  int* cnt;              // [n_phases + 1] completion counters: zero on entry, reset on exit
-  unsigned long long* dbg;  // optional [n_phases][4] %globaltimer timeline of CTA 0 (NULL: off)
+  KTrace kt;
 };
 
 struct QuantWArgs {

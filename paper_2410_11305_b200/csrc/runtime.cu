@@ -7,8 +7,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
-#include <map>
-#include <string>
+#include <algorithm>
 #include <vector>
 
 #include "../../include/qspec_b200.h"
@@ -32,25 +31,23 @@ cudaError_t launch_repack_ref(const uint8_t* ref_codes, const float* ref_scales,
 
 cudaError_t launch_control(int op, const SeqState& s, int j, cudaStream_t st);
 cudaError_t launch_add_rows(float* x, const float* y, int n, cudaStream_t st);
-cudaError_t launch_forward_mk(int L, int T, const MkArgs& g, int n_cta, cudaStream_t st);
-int mk_tmax_bucket(int T, int L);
-int mk_attn_chunk_len();
 }  // namespace qs
 
 using namespace qs;
 
 namespace qs {
-bool fuse_pack_enabled() {
-  static int on = -1;
-  if (on < 0) {
-#if QS_FUSED_PACK
-    const char* e = getenv("QS_FUSED_PACK_ON");  // experiment: operand pack as a pre-phase of the linear
-    on = (e && e[0] == '1') ? 1 : 0;
-#else
-    on = 0;  // fused pre-phase compiled out (QS_FUSED_PACK=0 in linear_tc.cu)
-#endif
-  }
-  return on == 1;
+static int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return (e && e[0]) ? atoi(e) : dflt;
+}
+// L2 look-ahead window of the forward's weight stream, MB (QS_PF_WINDOW_MB; 0 = off)
+int pf_window_mb() {
+  static int w = env_int("QS_PF_WINDOW_MB", 0);  // measured: a 32-96 MB window slows the step
+  return w;
+}
+int pf_own_enabled() {
+  static int on = env_int("QS_PF_OWN", 0);
+  return on;
 }
 bool pdl_enabled() {
   static int on = -1;
@@ -64,6 +61,19 @@ bool pdl_enabled() {
 
 static unsigned long long* g_dbg = nullptr;
 namespace {
+
+// qs_ktrace_*: per-launch slots of the device timeline (KTrace in qs_common.cuh)
+struct KTraceHost {
+  unsigned long long* buf = nullptr;
+  int cap = 0;
+  std::vector<int32_t> tags;
+} g_kt;
+
+KTrace next_trace(int32_t tag) {
+  if (g_kt.buf == nullptr || (int)g_kt.tags.size() >= g_kt.cap) return KTrace{nullptr, 0};
+  g_kt.tags.push_back(tag);
+  return KTrace{g_kt.buf, (int)g_kt.tags.size() - 1};
+}
 
 constexpr int kMaxT = 64;
 constexpr int kGbarOffset = 4096;  // grid-barrier words live past every per-tile counter
@@ -102,25 +112,18 @@ void prof_mark(cudaStream_t st, int32_t tag, bool begin) {
 }
 
 }  // namespace
-namespace qs {
-bool fuse_pack_enabled();
-}
 namespace {
 
-// Launch a linear whose operand comes from a.pk: either fused into the linear's
-// pre-phase (grid barrier) or as a separate act_pack launch overlapped via PDL.
+// Launch a linear whose operand comes from a.pk: a separate act_pack launch
+// overlapped via PDL, then the linear.
 cudaError_t launch_linear_packed(int L, LinearArgs& a, cudaStream_t st, int32_t tag = -1) {
   const int32_t mode_bits = 16 * (L == 1 ? 1 : 0);
-  cudaError_t e = cudaSuccess;
-  if (fuse_pack_enabled()) {
-    a.fuse_pack = 1;
-  } else {
-    a.fuse_pack = 0;
-    prof_mark(st, mode_bits + 5, true);  // kind 5: operand pack
-    e = launch_act_pack(L, a.pk, st);
-    prof_mark(st, 0, false);
-    if (e != cudaSuccess) return e;
-  }
+  prof_mark(st, mode_bits + 5, true);  // kind 5: operand pack
+  a.pk.kt = next_trace(mode_bits + 5);
+  cudaError_t e = launch_act_pack(L, a.pk, st);
+  prof_mark(st, 0, false);
+  if (e != cudaSuccess) return e;
+  a.kt = next_trace(tag >= 0 ? tag : mode_bits + 15);
   if (tag >= 0) prof_mark(st, tag, true);
   e = launch_linear(L, a, st);
   if (tag >= 0) prof_mark(st, 0, false);
@@ -187,9 +190,52 @@ LinearArgs linear_args(const qs_qweight_t& w, int T, int L, const qs_workspace_t
   a.ldo = ldo;
   a.arg_val = ws->arg_val;
   a.arg_idx = ws->arg_idx;
-  a.gbar = ws->counters + kGbarOffset;
+  a.pf_n = 0;
+  a.pf_own = pf_own_enabled();
   return a;
 }
+
+// The forward's weight stream in launch order (codes then scales of every linear).
+// Linear j prefetches the stream bytes [E_{j-1} + W, E_j + W) (mod the stream length:
+// the next forward of a decode loop streams the same weights), so every byte is
+// requested once, W bytes before the linear that consumes it starts.
+struct WeightStream {
+  std::vector<const uint8_t*> ptr;
+  std::vector<size_t> len;
+  std::vector<size_t> lin_end;  // stream offset after each linear
+  size_t total = 0;
+  void add_linear(const qs_qweight_t& w) {
+    const size_t cb = (size_t)w.n_tiles * w.n_chunks * kChunkBytes, sb = (size_t)w.n_tiles * w.n_chunks * kTileN * 4;
+    ptr.push_back(w.codes);
+    len.push_back(cb);
+    ptr.push_back(reinterpret_cast<const uint8_t*>(w.scales));
+    len.push_back(sb);
+    total += cb + sb;
+    lin_end.push_back(total);
+  }
+  // append the pieces of stream range [A, B) (A, B may exceed total: wrap) to a.pf_*
+  void ranges(LinearArgs& a, size_t A, size_t B) const {
+    a.pf_n = 0;
+    if (total == 0 || B <= A) return;
+    if (B - A > total) A = B - total;
+    while (A < B && a.pf_n < kMaxPf) {
+      const size_t a0 = A % total;
+      size_t off = 0, i = 0;
+      while (i < len.size() && off + len[i] <= a0) off += len[i++];
+      const size_t take = std::min(B - A, off + len[i] - a0);
+      a.pf_ptr[a.pf_n] = ptr[i] + (a0 - off);
+      a.pf_len[a.pf_n] = (uint32_t)take;
+      ++a.pf_n;
+      A += take;
+    }
+  }
+  void window(LinearArgs& a, int j) const {
+    const size_t W = (size_t)pf_window_mb() << 20;
+    if (W == 0) return;
+    const size_t prev = j == 0 ? 0 : lin_end[j - 1];
+    ranges(a, prev + W, lin_end[j] + W);
+  }
+};
 
 int check_weight(const qs_qweight_t* w) {
   if (!w || !w->codes || !w->scales) return QS_ERR_SHAPE;
@@ -253,6 +299,20 @@ int qs_profile_enable(int32_t max_launches) {
   g_prof.tag = new int32_t[max_launches];
   for (int i = 0; i < g_prof.cap; ++i)
     if (cudaEventCreate(&g_prof.ev[i]) != cudaSuccess) return QS_ERR_CUDA;
+  return QS_OK;
+}
+
+int qs_ktrace_enable(uint64_t* buf, int32_t cap) {
+  g_kt.buf = reinterpret_cast<unsigned long long*>(buf);
+  g_kt.cap = buf ? cap : 0;
+  g_kt.tags.clear();
+  return QS_OK;
+}
+
+int qs_ktrace_read(int32_t* tags, int32_t max_out, int32_t* n_out) {
+  const int n = (int)g_kt.tags.size() < max_out ? (int)g_kt.tags.size() : max_out;
+  for (int i = 0; i < n; ++i) tags[i] = g_kt.tags[i];
+  *n_out = n;
   return QS_OK;
 }
 
@@ -404,6 +464,25 @@ int qs_act_quant(const float* x, int32_t T, int32_t K, int32_t g, int8_t* codes,
   return status(launch_act_pack(1, p, (cudaStream_t)stream));
 }
 
+int qs_rmsnorm(const float* x, const float* w, int32_t T, int32_t K, float eps, float* y, void* stream) {
+  if (T < 1 || K < 1 || !x || !w || !y) return QS_ERR_SHAPE;
+  if (!(eps > 0.f)) return QS_ERR_SHAPE;
+  int g = K < 128 ? K : 128;  // any group size works: only the normalised row is written
+  while (K % g) --g;
+  PackArgs p{};
+  p.x = x;
+  p.ldx = K;
+  p.T = T;
+  p.K = K;
+  p.g = g;
+  p.gp = round_up(g, kChunkK);
+  p.G = K / g;
+  p.rms_w = w;
+  p.eps = eps;
+  p.y_out = y;
+  return status(launch_act_pack(1, p, (cudaStream_t)stream));
+}
+
 int qs_w4a4_linear(const qs_qweight_t* w, const float* x, int32_t T, float* y, const qs_workspace_t* ws,
                    void* stream) {
   return run_linear(w, x, T, y, ws, 1, kOpStore, nullptr, (cudaStream_t)stream);
@@ -466,6 +545,15 @@ int forward_impl(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const q
   const int att_cmax = attention_chunks(m->rope_len);
   if (attention_smem_bytes(b->blk_qmax, hpk, hd, b->ctx_cap) > 200 * 1024) return QS_ERR_SHAPE;
   cudaError_t e;
+  WeightStream ws_stream;
+  for (int li = 0; li < m->n_layers; ++li) {
+    ws_stream.add_linear(m->layers[li].qkv);
+    ws_stream.add_linear(m->layers[li].o);
+    ws_stream.add_linear(m->layers[li].gate_up);
+    ws_stream.add_linear(m->layers[li].down);
+  }
+  ws_stream.add_linear(m->lm_head);
+  int lin_j = 0;
   for (int li = 0; li < m->n_layers; ++li) {
     const qs_layer_t& ly = m->layers[li];
     // q|k|v projection; operand = rmsnorm(x) (+ embedding gather on layer 0), fused
@@ -492,6 +580,7 @@ int forward_impl(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const q
     a.block_table = m->block_table;
     a.bt_ld = m->bt_ld;
     a.page = m->page;
+    ws_stream.window(a, lin_j++);
     if ((e = launch_linear_packed(L, a, st, mode * 16 + 0)) != cudaSuccess) return status(e);
     // attention (model.py:293-330), split-KV partials
     AttnArgs at{};
@@ -519,6 +608,7 @@ int forward_impl(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const q
     at.part_ml = ws->att_ml;
     at.cmax = att_cmax;
     prof_mark(st, mode * 16 + 6, true);  // kind 6: attention
+    at.kt = next_trace(mode * 16 + 6);
     if ((e = launch_attention(at, b->n_blk, st)) != cudaSuccess) return status(e);
     prof_mark(st, 0, false);
     // o_proj + residual (model.py:332); its fused pre-phase merges the attention chunks
@@ -530,6 +620,7 @@ int forward_impl(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const q
     a.pk.att_hd = hd;
     a.pk.att_cmax = att_cmax;
     a.pk.att_chunk = attention_chunk_len();
+    ws_stream.window(a, lin_j++);
     if ((e = launch_linear_packed(L, a, st, mode * 16 + 1)) != cudaSuccess) return status(e);
     if (tp) {
       const int rc = reduce_into_x();
@@ -540,10 +631,12 @@ int forward_impl(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const q
     a.pk = pack_args(ly.gate_up, ws->x, d, T, ws, L);
     a.pk.rms_w = ly.ffn_norm;
     a.pk.eps = m->norm_eps;
+    ws_stream.window(a, lin_j++);
     if ((e = launch_linear_packed(L, a, st, mode * 16 + 2)) != cudaSuccess) return status(e);
     // down_proj + residual (model.py:336)
     a = linear_args(ly.down, T, L, ws, res_op, res_out, d);
     a.pk = pack_args(ly.down, ws->h, ff, T, ws, L);
+    ws_stream.window(a, lin_j++);
     if ((e = launch_linear_packed(L, a, st, mode * 16 + 3)) != cudaSuccess) return status(e);
     if (tp) {
       const int rc = reduce_into_x();
@@ -556,6 +649,7 @@ int forward_impl(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const q
   a.pk.rms_w = m->final_norm;
   a.pk.eps = m->norm_eps;
   a.argmax_out = argmax;
+  ws_stream.window(a, lin_j++);
   e = launch_linear_packed(L, a, st, mode * 16 + 4);
   return status(e);
 }
@@ -576,189 +670,6 @@ int qs_forward_tp(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const 
 }
 
 }  // extern "C"
-
-// ---------------------------------------------------------------- persistent forward
-// The phase program of one forward (model.py:255-348) for the persistent kernel
-// (forward_mk.cu): the same arguments qs_forward passes to its per-step launches,
-// plus the dependency edges between phases.  Programs are cached by content
-// (they hold only pointers and shapes), so a CUDA-graph capture replays a
-// program built -- and copied to the device -- during the warm-up call.
-namespace {
-struct MkProgram {
-  MkPhase* d_prog = nullptr;
-  int* d_lin = nullptr;
-  int* d_cnt = nullptr;
-  int n_phases = 0, n_lin = 0;
-};
-std::map<std::string, MkProgram> g_mk_cache;
-
-int mk_supported(const qs_model_t* m, const qs_batch_t* b) {
-  const int hd = m->d_model / m->n_heads;
-  if (hd % 4 != 0 || hd > 128) return 0;
-  if (attention_chunk_len() != mk_attn_chunk_len()) return 0;
-  if (m->page < 8) return 0;                                // <= 8 pages per 64-key chunk
-  if (b->blk_qmax * (m->n_heads / m->n_kv_heads) > 16) return 0;  // queries per attention item
-
-  return 1;
-}
-}  // namespace
-
-extern "C" int qs_forward_mk(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const qs_workspace_t* ws,
-                             float* logits, int32_t* argmax, void* stream) {
-  cudaStream_t st = (cudaStream_t)stream;
-  const int T = b->T;
-  if (T < 1 || T > kMaxT) return QS_ERR_SHAPE;
-  const int L = mode == QS_MODE_LOW ? 1 : 3;
-  const int d = m->d_model, H = m->n_heads, KV = m->n_kv_heads, hd = d / H, ff = m->d_ff;
-  const int hpk = H / KV;
-  if (b->blk_qmax * hpk > 64 || hd % 4 != 0) return QS_ERR_SHAPE;
-  if (b->ctx_cap > m->rope_len) return QS_ERR_OVERFLOW;
-  if (!mk_supported(m, b)) return qs_forward(m, b, mode, ws, logits, argmax, stream);
-  const int att_cmax = attention_chunks(m->rope_len);
-  const int grid = num_sms();
-  std::vector<MkPhase> prog;
-  std::vector<int> lin;
-  auto add = [&](const MkPhase& p) {
-    prog.push_back(p);
-    if (p.kind == kMkLin) lin.push_back((int)prog.size() - 1);
-    return (int)prog.size() - 1;
-  };
-  auto pack_phase = [&](const PackArgs& pk, int dep, int dep_count) {
-    MkPhase p;
-    memset(&p, 0, sizeof(p));
-    p.kind = kMkPack;
-    p.dep = dep;
-    p.dep_count = dep_count;
-    p.pk = pk;
-    return add(p);
-  };
-  auto lin_phase = [&](const LinearArgs& a, int dep) {
-    MkPhase p;
-    memset(&p, 0, sizeof(p));
-    p.kind = kMkLin;
-    p.dep = dep;
-    p.dep_count = grid;
-    p.lin = a;
-    p.lin.pk = PackArgs{};
-    return add(p);
-  };
-  int prev = -1, prev_count = 0;
-  for (int li = 0; li < m->n_layers; ++li) {
-    const qs_layer_t& ly = m->layers[li];
-    PackArgs pk = pack_args(ly.qkv, ws->x, d, T, ws, L);
-    pk.rms_w = ly.attn_norm;
-    pk.eps = m->norm_eps;
-    if (li == 0) {
-      pk.gather_ids = b->tokens;
-      pk.emb = m->tok_emb;
-      pk.x_out = ws->x;
-    }
-    int p = pack_phase(pk, prev, prev_count);
-    LinearArgs a = linear_args(ly.qkv, T, L, ws, kOpQkvRope, ws->q, H * hd);
-    a.pos = b->positions;
-    a.slot = b->slots;
-    a.rope_cos = m->rope_cos;
-    a.rope_sin = m->rope_sin;
-    a.hd = hd;
-    a.n_q = H * hd;
-    a.n_k = KV * hd;
-    a.n_kv_heads = KV;
-    a.kcache = ly.k_cache;
-    a.vcache = ly.v_cache;
-    a.block_table = m->block_table;
-    a.bt_ld = m->bt_ld;
-    a.page = m->page;
-    const int p_qkv = lin_phase(a, p);
-    MkPhase at;
-    memset(&at, 0, sizeof(at));
-    at.kind = kMkAttn;
-    at.dep = p_qkv;
-    at.dep_count = ly.qkv.n_tiles;
-    at.n_blk = b->n_blk;
-    AttnArgs& t = at.at;
-    t.q = ws->q;
-    t.ldq = H * hd;
-    t.kcache = ly.k_cache;
-    t.vcache = ly.v_cache;
-    t.block_table = m->block_table;
-    t.bt_ld = m->bt_ld;
-    t.page = m->page;
-    t.pos = b->positions;
-    t.slot = b->slots;
-    t.blk_tok0 = b->blk_tok0;
-    t.blk_ntok = b->blk_ntok;
-    t.H = H;
-    t.KV = KV;
-    t.hd = hd;
-    t.hpk = hpk;
-    t.inv_sqrt_hd = 1.0f / sqrtf((float)hd);
-    t.qmax = b->blk_qmax;
-    t.ctx_cap = b->ctx_cap;
-    t.out = ws->attn;
-    t.ldo = d;
-    t.part_o = ws->att_o;
-    t.part_ml = ws->att_ml;
-    t.cmax = att_cmax;
-    const int p_att = add(at);
-    pk = pack_args(ly.o, ws->attn, d, T, ws, L);
-    pk.att_o = ws->att_o;
-    pk.att_ml = ws->att_ml;
-    pk.att_pos = b->positions;
-    pk.att_hd = hd;
-    pk.att_cmax = att_cmax;
-    pk.att_chunk = attention_chunk_len();
-    p = pack_phase(pk, p_att, grid);
-    const int p_o = lin_phase(linear_args(ly.o, T, L, ws, kOpResidual, ws->x, d), p);
-    pk = pack_args(ly.gate_up, ws->x, d, T, ws, L);
-    pk.rms_w = ly.ffn_norm;
-    pk.eps = m->norm_eps;
-    p = pack_phase(pk, p_o, ly.o.n_tiles);
-    const int p_gu = lin_phase(linear_args(ly.gate_up, T, L, ws, kOpSiluMul, ws->h, ff), p);
-    p = pack_phase(pack_args(ly.down, ws->h, ff, T, ws, L), p_gu, ly.gate_up.n_tiles);
-    prev = lin_phase(linear_args(ly.down, T, L, ws, kOpResidual, ws->x, d), p);
-    prev_count = ly.down.n_tiles;
-  }
-  PackArgs pk = pack_args(m->lm_head, ws->x, d, T, ws, L);
-  pk.rms_w = m->final_norm;
-  pk.eps = m->norm_eps;
-  const int p = pack_phase(pk, prev, prev_count);
-  LinearArgs a = linear_args(m->lm_head, T, L, ws, kOpLogits, logits, m->vocab);
-  a.argmax_out = argmax;
-  lin_phase(a, p);
-
-  // the persistent kernel's image height (its own token buckets)
-  const int r_pad = img_rows(mk_tmax_bucket(T, L), L);
-  for (MkPhase& ph : prog) {
-    if (ph.kind == kMkPack) ph.pk.r_pad = r_pad;
-    if (ph.kind == kMkLin) ph.lin.r_pad = r_pad;
-  }
-  std::string key(reinterpret_cast<const char*>(prog.data()), prog.size() * sizeof(MkPhase));
-  key.append(reinterpret_cast<const char*>(&grid), sizeof(grid));
-  auto itp = g_mk_cache.find(key);
-  if (itp == g_mk_cache.end()) {
-    MkProgram mp;
-    mp.n_phases = (int)prog.size();
-    mp.n_lin = (int)lin.size();
-    cudaError_t e;
-    if ((e = cudaMalloc(&mp.d_prog, prog.size() * sizeof(MkPhase))) != cudaSuccess) return status(e);
-    if ((e = cudaMalloc(&mp.d_lin, lin.size() * sizeof(int))) != cudaSuccess) return status(e);
-    if ((e = cudaMalloc(&mp.d_cnt, (prog.size() + 1) * sizeof(int))) != cudaSuccess) return status(e);
-    if ((e = cudaMemcpy(mp.d_prog, prog.data(), prog.size() * sizeof(MkPhase), cudaMemcpyHostToDevice)) !=
-        cudaSuccess)
-      return status(e);
-    if ((e = cudaMemcpy(mp.d_lin, lin.data(), lin.size() * sizeof(int), cudaMemcpyHostToDevice)) != cudaSuccess)
-      return status(e);
-    if ((e = cudaMemset(mp.d_cnt, 0, (prog.size() + 1) * sizeof(int))) != cudaSuccess) return status(e);
-    if ((e = cudaDeviceSynchronize()) != cudaSuccess) return status(e);
-    itp = g_mk_cache.emplace(key, mp).first;
-  }
-  const MkProgram& mp = itp->second;
-  MkArgs g{mp.d_prog, mp.n_phases, mp.d_lin, mp.n_lin, mp.d_cnt, g_dbg};
-  prof_mark(st, mode * 16 + 7, true);  // kind 7: whole persistent forward
-  cudaError_t e = launch_forward_mk(L, T, g, grid, st);
-  prof_mark(st, 0, false);
-  return status(e);
-}
 
 extern "C" {
 int qs_draft_prep(const qs_seq_t* s, int32_t step, void* stream) {

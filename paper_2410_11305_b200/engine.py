@@ -18,7 +18,6 @@ the reference's serving loop (serving.py:1-9).
 from __future__ import annotations
 
 import ctypes
-import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -43,7 +42,7 @@ class SlotResult:
 class DecodeEngine:
     def __init__(self, model: TransformerModel, batch: int, *, gamma: int = 3, max_new_cap: int = 256,
                  eos_token: int | None = None, draft_low: bool = True, algorithm: str = "qspec",
-                 greedy_low: bool = False, use_graphs: bool = True, persistent: bool | None = None) -> None:
+                 greedy_low: bool = False, use_graphs: bool = True) -> None:
         import torch
         _lib.require_cuda()
         if gamma < 1:
@@ -80,12 +79,6 @@ class DecodeEngine:
         self.draft_batches = self._batches(1)
         self.verify_batches = self._batches(G1)
         self.use_graphs = use_graphs
-        # persistent=True: one forward_mk launch per forward; False (default for now): the
-        # per-step launch sequence (qs_forward).  Results are bit-identical.
-        if persistent is None:
-            persistent = os.environ.get("QSPEC_PERSISTENT", "0") == "1"
-        self.persistent = persistent
-        self._fwd_fn = "qs_forward_mk" if persistent else "qs_forward"
         self.graph = None
         self.n_launch_cycle = 0
 
@@ -112,7 +105,7 @@ class DecodeEngine:
         mode = _lib.QS_MODE_LOW if low else _lib.QS_MODE_HIGH
         st = _lib.stream_ptr()
         for b, off in batches:
-            _lib.call(self._fwd_fn, self.cm, b, mode, self.ws, None, self.t["argmax"].data_ptr() + off, st)
+            _lib.call("qs_forward", self.cm, b, mode, self.ws, None, self.t["argmax"].data_ptr() + off, st)
 
     # ------------------------------------------------------------------ step bodies
     def _cycle_body(self) -> None:
@@ -133,8 +126,8 @@ class DecodeEngine:
     def launches_per_step(self) -> int:
         """Kernels one step launches (for the bench's gpu_launches claim)."""
         L = self.cfg.n_layers
-        # per layer: 4 packs, 4 linears, attention; + final pack + lm_head -- or one persistent launch
-        fwd = 1 if self.persistent else 9 * L + 2
+        # per layer: 4 packs, 4 linears, attention; + final pack + lm_head
+        fwd = 9 * L + 2
         if self.algorithm == "qspec":
             return self.gamma * (1 + fwd * len(self.draft_batches)) + 1 + fwd * len(self.verify_batches) + 1
         return 2 + fwd * len(self.draft_batches)

@@ -21,6 +21,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import threading
 from dataclasses import dataclass, field
 from enum import Enum
 
@@ -178,9 +179,12 @@ class TransformerModel:
         return m
 
     def workspace(self, t_max: int = 64):
-        """Cached per-model scratch (allocated once; the kernels leave counters zeroed)."""
+        """Cached scratch per (model, thread, device) -- allocated once; the kernels leave
+        counters zeroed.  Engines over one shared model may run in threads,
+        so no two threads ever share a workspace."""
         import torch
-        if t_max not in self._ws_cache:
+        key = (t_max, threading.get_ident(), torch.cuda.current_device())
+        if key not in self._ws_cache:
             probe = _lib.Model(n_layers=self.config.n_layers, d_model=self.config.d_model,
                                n_heads=self.config.n_heads, n_kv_heads=self.config.n_kv_heads,
                                d_ff=self.config.d_ff, vocab=self.config.vocab_size,
@@ -190,8 +194,8 @@ class TransformerModel:
             bufs = {n: torch.zeros(max(16, getattr(sizes, n)), dtype=torch.uint8, device="cuda")
                     for n, _ in _lib.WorkspaceSizes._fields_}
             ws = _lib.Workspace(**{n: b.data_ptr() for n, b in bufs.items()})
-            self._ws_cache[t_max] = (ws, bufs)
-        return self._ws_cache[t_max]
+            self._ws_cache[key] = (ws, bufs)
+        return self._ws_cache[key]
 
 
 class WriteTarget(Enum):
@@ -327,16 +331,25 @@ class _BatchBuffers:
         self.arg = torch.zeros(64, dtype=torch.int32, device="cuda")
 
 
-_bb = None
+_tls = threading.local()  # staging buffers per (thread, device): engines may run in threads
+
+
+def _batch_buffers() -> _BatchBuffers:
+    import torch
+    per = getattr(_tls, "bb", None)
+    if per is None:
+        per = _tls.bb = {}
+    dev = torch.cuda.current_device()
+    if dev not in per:
+        per[dev] = _BatchBuffers()
+    return per[dev]
 
 
 def run_forward_chunks(model: TransformerModel, kv: KVCache, ids: list[int], base: int, low: bool,
                        slot: int = 0):
     """Enqueue qs_forward over ``ids`` at positions base.. (chunks of <= 64 tokens)."""
     import torch
-    global _bb
-    if _bb is None:
-        _bb = _BatchBuffers()
+    _bb = _batch_buffers()
     cfg = model.config
     hpk = cfg.n_heads // cfg.n_kv_heads
     tmax = min(64, max(1, 64 // hpk), 8192 // (hpk * cfg.head_dim) or 1)

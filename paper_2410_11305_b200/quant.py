@@ -18,6 +18,8 @@ surface (one instance per linear, shared by both modes) is preserved.
 
 from __future__ import annotations
 
+import threading
+
 from dataclasses import dataclass, field
 from enum import Enum
 
@@ -255,7 +257,20 @@ def C_byref(x):
     return ctypes.byref(x)
 
 
-_ws = _LinearWorkspace()
+class _ThreadWorkspaces(threading.local):
+    """One _LinearWorkspace per (thread, device): standalone qlinear_forward calls from
+    several threads never share staging buffers."""
+
+    def get(self, n: int, k: int, g: int):
+        import torch
+        per = self.__dict__.setdefault("per", {})
+        dev = torch.cuda.current_device()
+        if dev not in per:
+            per[dev] = _LinearWorkspace()
+        return per[dev].get(n, k, g)
+
+
+_ws = _ThreadWorkspaces()
 
 
 def qlinear_forward(q: QuantizedTensor, x, mode: ExecutionMode):

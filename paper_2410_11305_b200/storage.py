@@ -258,6 +258,13 @@ def load_checkpoint(path: str) -> TransformerModel:
     import torch
     from .errors import CheckpointError
     cfg, recs = read_checkpoint(path)
+    # quant.py:138-139, reported by storage.py:390-397 as a CheckpointError naming the
+    # codes record: every quantized store's scales must be finite and non-negative
+    for name, (dtype, _, payload) in recs.items():
+        if name.endswith(".scales") and name[:-7] + ".codes" in recs and dtype == _F32:
+            sc = np.frombuffer(payload, dtype="<f4")
+            if np.any(sc < 0) or not np.all(np.isfinite(sc)):
+                raise CheckpointError(f"record '{name[:-7]}.codes': scales must be finite and non-negative")
     _lib.require_cuda()
     hd, g = cfg.head_dim, cfg.group_size
 
@@ -280,9 +287,9 @@ def load_checkpoint(path: str) -> TransformerModel:
         if dtype != _I4 or shape != (n, k):
             raise CheckpointError(f"record '{cname}': expected i4-packed ({n}, {k}), found dtype={dtype} "
                                   f"shape={shape}")
+        scales = take_f32(f"{name}.scales", (n, k // g))
         codes = torch.from_numpy(np.frombuffer(payload, dtype=np.uint8).copy()).cuda()
-        scales = take_f32(f"{name}.scales", (n, k // g)).cuda()
-        return codes, scales
+        return codes, scales.cuda()
 
     layers, lm, emb = _empty_model(cfg)
     emb.copy_(take_f32("token_embedding", (cfg.vocab_size, cfg.d_model)))

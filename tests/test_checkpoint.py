@@ -56,3 +56,19 @@ def test_load_equals_random_init_and_saves_byte_identical(tmp_path):
     prompt = [5, 9, 100, 3, 77]
     cfg = Q.GenerationConfig(gamma=3, max_new_tokens=16)
     assert Q.generate_qspec(m, prompt, cfg).new_tokens == Q.generate_qspec(r, prompt, cfg).new_tokens
+
+
+@pytest.mark.parametrize("bad", [float("nan"), float("inf"), -0.5])
+def test_corrupt_scales_rejected(tmp_path, bad):
+    # quant.py:138-139 + storage.py:390-397: a NaN / infinite / negative scale is a
+    # CheckpointError naming the record, raised before any device work
+    data = bytearray(open(CKPT, "rb").read())
+    _, recs = S.read_checkpoint(CKPT)
+    payload = recs["layers.1.down_proj.scales"][2]
+    off = bytes(data).find(payload)
+    assert off > 0
+    data[off + 8:off + 12] = np.array([bad], dtype="<f4").tobytes()
+    p = tmp_path / "bad.qspc"
+    p.write_bytes(bytes(data))
+    with pytest.raises(Q.CheckpointError, match="layers.1.down_proj.codes"):
+        S.load_checkpoint(str(p))

@@ -126,3 +126,73 @@ def test_acceptance_shapes(golden, mi):
         ref = [int(t) for t in golden[f"spec{mi}.p{pi}.greedy"]]
         assert O.generate(m, p, max_new=12, qspec=False).new_tokens == ref
         assert O.generate(m, p, gamma=3, max_new=12).new_tokens == ref
+
+
+@pytest.mark.parametrize("n", [1, 5, 7, 8, 13, 64, 96, 127, 128, 200, 256, 1000, 4096, 5120])
+def test_pairwise_sum_is_numpys_mean_order(n):
+    # the device RMSNorm implements O.pairwise_sum_f32's order (csrc/pack_dev.cuh); pin it
+    # to np.mean(x*x, dtype=float32) of numerics.py:60 on rows where the order matters
+    rng = np.random.default_rng(n)
+    x = (rng.standard_normal((6, n)) * rng.uniform(0.01, 50, size=(6, 1))).astype(np.float32)
+    ref = np.mean(x * x, axis=-1, keepdims=True, dtype=np.float32)[:, 0]
+    got = np.array([O.pairwise_sum_f32(r * r) / np.float32(n) for r in x], dtype=np.float32)
+    assert got.tobytes() == ref.tobytes()
+
+
+def test_pairwise_order_is_discriminating():
+    # a plain sequential fp32 sum disagrees with numpy on 4096-wide rows (the 7B d_model):
+    # the test above would catch a device reduction in the wrong order
+    rng = np.random.default_rng(1)
+    x = (rng.standard_normal((64, 4096)) * 3).astype(np.float32)
+    ref = np.mean(x * x, axis=-1, dtype=np.float32)
+    seq = []
+    for r in x:
+        acc = np.float32(0)
+        for v in (r * r):
+            acc = np.float32(acc + v)
+        seq.append(np.float32(acc / np.float32(4096)))
+    assert (np.array(seq, dtype=np.float32) != ref).any()
+
+
+def test_long_context_streams():
+    # tests/golden/large_ctx.npz: C0 tiny with 270-token prompts (>= 5 split-KV chunks)
+    import os
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "large_ctx.npz"))
+    m = O.random_model(O.OracleConfig(**dict(TINY, max_seq_len=400)), 0)
+    for i in (0, 5):
+        p = [int(t) for t in g[f"p{i}.prompt"]]
+        gr = O.generate(m, p, max_new=40, qspec=False)
+        assert gr.new_tokens == [int(t) for t in g[f"p{i}.greedy_high"]]
+        qs = O.generate(m, p, gamma=3, max_new=40)
+        assert qs.tokens == gr.tokens
+        assert [c[1] for c in qs.cycles] == [int(a) for a in g[f"p{i}.qspec_accept_lens"]]
+        assert qs.acceptance_rate == g[f"p{i}.qspec_stats"][0] and qs.tokens_per_cycle == g[f"p{i}.qspec_stats"][1]
+        low = O.generate(m, p, max_new=40, qspec=False, low_greedy=True)
+        assert low.new_tokens == [int(t) for t in g[f"p{i}.greedy_low"]]
+
+
+def test_low_path_is_order_sensitive():
+    # The reference's W4A4 forward with float64-accurate linear sums (what a device
+    # integer core computes, up to its fp32 epilogue) instead of einsum's sequential
+    # float32 sums: identical W4A16 tokens, but the W4A4 greedy stream parts ways within
+    # a few tokens on this 270-token prompt -- one flipped activation code cascades.
+    # This is why draft-stream parity is statistical (tests/test_gpu_draft_parity.py).
+    import os
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "large_ctx.npz"))
+    m = O.random_model(O.OracleConfig(**dict(TINY, max_seq_len=400)), 0)
+    p = [int(t) for t in g["p0.prompt"]]
+    ref_low = [int(t) for t in g["p0.greedy_low"]]
+    orig = O.qlinear
+
+    def f64_sums(lin, x, low):
+        xq = O.fake_quant(x, lin.g) if low else x
+        return (xq.astype(np.float64) @ lin.wt.astype(np.float64)).astype(np.float32)
+
+    try:
+        O.qlinear = f64_sums
+        hi = O.generate(m, p, max_new=40, qspec=False).new_tokens
+        lo = O.generate(m, p, max_new=40, qspec=False, low_greedy=True).new_tokens
+    finally:
+        O.qlinear = orig
+    assert hi == [int(t) for t in g["p0.greedy_high"]]
+    assert lo[:3] == ref_low[:3] and lo != ref_low
