@@ -128,14 +128,22 @@ def run_decode(model, a, batch: int, algorithm: str, prompts: np.ndarray, steps:
     import torch
     from paper_2410_11305_b200.engine import DecodeEngine
     eng = DecodeEngine(model, batch, gamma=a.gamma, max_new_cap=a.new + 8, algorithm=algorithm)
+    # prefill (reported separately, excluded from the decode rate): every
+    # prompt through the W4A16 path, device-timed on the launch stream
+    st = torch.cuda.current_stream()
+    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    p0.record(st)
     for b in range(batch):
         eng.prefill(b, [int(t) for t in prompts[b]], a.new)
+    p1.record(st)
+    torch.cuda.synchronize()
+    prefill_ms = p0.elapsed_time(p1)
     for _ in range(warmup):
         eng.step()
     torch.cuda.synchronize()
     n0 = eng.t["n_out"].sum().item()
     nd0, na0 = eng.t["n_drafted"].sum().item(), eng.t["n_accepted"].sum().item()
-    st = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if dist is not None:
         dist.barrier()
@@ -155,7 +163,9 @@ def run_decode(model, a, batch: int, algorithm: str, prompts: np.ndarray, steps:
     nd, na = eng.t["n_drafted"].sum().item() - nd0, eng.t["n_accepted"].sum().item() - na0
     out = {"ms": ms, "tokens": tokens, "steps": steps, "tok_s": tokens / (ms / 1e3),
            "acceptance_rate": (na / nd) if nd else None, "launches_per_step": eng.launches_per_step(),
-           "clocks": ck}
+           "clocks": ck,
+           "prefill": {"tokens": int(prompts[:batch].size), "ms": round(prefill_ms, 3),
+                       "tok_s": round(prompts[:batch].size / (prefill_ms / 1e3), 1)}}
     # per-cycle accept lengths of every slot (trace[b][cycle][1]) for the cost model
     ncyc = eng.t["n_cycles"].cpu().numpy()
     tr = eng.t["trace"].reshape(batch, -1, 4).cpu().numpy()
@@ -168,7 +178,7 @@ def run_decode(model, a, batch: int, algorithm: str, prompts: np.ndarray, steps:
     return out
 
 
-def run_e2e(model, a, batch: int, prompts: np.ndarray) -> dict:
+def run_e2e(model, a, batch: int, prompts: np.ndarray, dist=None) -> dict:
     """Public-API end to end: pinned host prompts -> device -> QSpec cycles -> tokens on the host."""
     import torch
     from paper_2410_11305_b200.engine import DecodeEngine
@@ -177,6 +187,8 @@ def run_e2e(model, a, batch: int, prompts: np.ndarray) -> dict:
     eng.prefill(0, [int(t) for t in prompts[0]], a.new)   # warm the graph once
     eng.step()
     torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
     t0 = time.perf_counter()
     dev = host.cuda(non_blocking=True)
     for b in range(batch):
@@ -197,8 +209,14 @@ def run_e2e(model, a, batch: int, prompts: np.ndarray) -> dict:
     h2d = host.numel() * 4
     d2h = cycles * flags.numel() * 4 + toks * 4
     del eng
-    return {"value": toks / wall, "unit": UNIT, "h2d_bytes_per_step": h2d / cycles, "d2h_bytes_per_step": d2h / cycles,
-            "cycles": cycles, "tokens": toks, "wall_s": wall}
+    # whole job at N > 1: tokens summed over ranks / the slowest rank's wall time
+    from paper_2410_11305_b200.replicas import reduce_throughput
+    toks_all, wall_ms = reduce_throughput(toks, wall * 1e3, dist)
+    wall_all = wall_ms / 1e3
+    return {"value": toks_all / wall_all, "unit": UNIT, "h2d_bytes_per_step": h2d / cycles,
+            "d2h_bytes_per_step": d2h / cycles, "cycles": cycles, "tokens": int(toks_all), "wall_s": wall_all,
+            "includes": "host->device prompt copy, prefill (W4A16), QSpec cycles, per-cycle done-flag reads, "
+                        "device->host tokens"}
 
 
 def forward_bytes(model, T: int, ctx_sum: float) -> float:
@@ -323,8 +341,17 @@ def cpu_reference(a, accept_rate: float | None, n_procs: int | None = None) -> d
     import multiprocessing as mp
     cfg_kw = model_cfg(a)
     L = cfg_kw["n_layers"]
-    cores = os.cpu_count() or 1
-    n_procs = n_procs or max(1, min(8, cores))
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    if n_procs is None:
+        # one single-threaded process per host core, bounded by memory: a 1-layer 7B-shape
+        # oracle model with its fp32 dequant caches needs ~2 GB (8B shape: ~3 GB)
+        per = (3 if a.model == "8b" else 2) << 30
+        try:
+            import psutil
+            avail = psutil.virtual_memory().available
+        except Exception:  # noqa: BLE001
+            avail = per * cores
+        n_procs = max(1, min(cores, int(0.8 * avail) // per))
     ctx = a.prompt + a.new // 2
     t0 = time.perf_counter()
     with mp.get_context("spawn").Pool(n_procs) as pool:
@@ -337,7 +364,7 @@ def cpu_reference(a, accept_rate: float | None, n_procs: int | None = None) -> d
     for f_d, f_v, h_d, h_v in res:
         cyc = a.gamma * ((f_d - h_d) * L + h_d) + ((f_v - h_v) * L + h_v)
         rates.append(tok_per_cycle / cyc)
-    return {"value": round(sum(rates), 4), "unit": UNIT, "cores": n_procs, "kind": "port",
+    return {"value": round(sum(rates), 4), "unit": UNIT, "cores": n_procs, "host_cores": cores, "kind": "port",
             "sample": (f"oracle port (bit-exact with pkg/src/qspec) of one {a.gamma}-draft QSpec cycle: 1 decoder layer "
                        f"+ lm_head of the 7B shape timed per forward kind (W4A4 draft M=1, W4A16 verify M={a.gamma + 1}, "
                        f"context {ctx}) and extrapolated to {L} layers; tokens/cycle from acceptance {p:.3f}; "
@@ -392,20 +419,24 @@ def main() -> None:
     ar_tokens, ar_ms = reduce_throughput(main_ar["tokens"], main_ar["ms"], dist)
 
     per_batch = {}
-    if rank == 0 and world == 1:
-        for b in sweep:
-            if b == a.batch:
-                q, r = main_q, main_ar
-            else:
-                q = run_decode(model, a, b, "qspec", prompts, a.steps, a.warmup)
-                r = run_decode(model, a, b, "greedy", prompts, a.steps, a.warmup)
-            per_batch[str(b)] = {"qspec_tok_s": round(q["tok_s"], 1), "w4a16_ar_tok_s": round(r["tok_s"], 1),
-                                 "speedup_vs_ar": round(q["tok_s"] / r["tok_s"], 3),
+    for b in sweep:   # every rank runs the sweep; whole-job rates (sum of tokens / max device time)
+        if b == a.batch:
+            q, r = main_q, main_ar
+        else:
+            q = run_decode(model, a, b, "qspec", prompts, a.steps, a.warmup, dist)
+            r = run_decode(model, a, b, "greedy", prompts, a.steps, a.warmup, dist)
+        qt, qm = reduce_throughput(q["tokens"], q["ms"], dist)
+        rt, rm = reduce_throughput(r["tokens"], r["ms"], dist)
+        q_rate, r_rate = qt / (qm / 1e3), rt / (rm / 1e3)
+        if rank == 0:
+            per_batch[str(b)] = {"qspec_tok_s": round(q_rate, 1), "w4a16_ar_tok_s": round(r_rate, 1),
+                                 "speedup_vs_ar": round(q_rate / r_rate, 3),
                                  "acceptance_rate": round(q["acceptance_rate"], 4),
                                  "tokens_per_cycle": round(q["tokens"] / (q["steps"] * b), 3),
-                                 "ms_per_cycle": round(q["ms"] / q["steps"], 3),
-                                 "ms_per_ar_step": round(r["ms"] / r["steps"], 3)}
-    e2e = run_e2e(model, a, a.batch, prompts)
+                                 "ms_per_cycle": round(qm / q["steps"], 3),
+                                 "ms_per_ar_step": round(rm / r["steps"], 3),
+                                 "prefill_tok_s": q["prefill"]["tok_s"]}
+    e2e = run_e2e(model, a, a.batch, prompts, dist)
     # reference cost model (costmodel.py:237-257) fed with a MEASURED latency profile
     from paper_2410_11305_b200.costmodel import (AcceptanceModel, analytic_speedup, geometric_acceptance,
                                                  measure_profile)
@@ -439,6 +470,8 @@ def main() -> None:
         "w4a16_ar_tokens_per_s": round(ar_tokens / (ar_ms / 1e3), 2),
         "speedup_vs_w4a16_ar": round(value / (ar_tokens / (ar_ms / 1e3)), 4),
         "acceptance_rate": round(main_q["acceptance_rate"], 4),
+        "value_per_gpu": round(value / world, 2),
+        "prefill": main_q["prefill"],
         "per_batch": per_batch,
         "roofline": roof,
         "cpu_baseline": cpu,

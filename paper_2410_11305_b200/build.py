@@ -15,8 +15,9 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-BUILD = os.path.join(HERE, "_build")
-LIB = os.path.join(HERE, "libqspec_b200.so")
+# QS_BUILD_DIR / QS_LIB_OUT: research variants (e.g. ablation builds) go elsewhere
+BUILD = os.environ.get("QS_BUILD_DIR") or os.path.join(HERE, "_build")
+LIB = os.environ.get("QS_LIB_OUT") or os.path.join(HERE, "libqspec_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",

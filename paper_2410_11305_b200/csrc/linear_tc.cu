@@ -46,6 +46,12 @@
 #ifndef QS_ONE_ACC
 #define QS_ONE_ACC 0
 #endif
+// research ablations (scripts/lin_ablate.sh), 0 in the product build; bit 0: unpack skips
+// LDS + ALU, 1: no MMAs (commits only), 2: epilogue skips TMEM loads + math, 3: unpack
+// skips tcgen05.st, 4: no weight bulk copies (the ring fills without HBM traffic)
+#ifndef QS_AB
+#define QS_AB 0
+#endif
 
 namespace qs {
 
@@ -94,7 +100,17 @@ struct LinCfg {
   static_assert(kStages >= 2, "pipeline depth");
   static_assert(kStages % kUnpackHalves == 0, "unpack groups must own whole weight slots");
   static constexpr int kSStages = kStages + 2;
-  static constexpr int kSEntry = kCPS * (128 + (TMAX < 8 ? 8 : TMAX)) * 4;  // ascale rows are a_ld = roundup(T, 8)
+  // Offset-binary weights (qs_common.cuh): small-token buckets feed the tensor core the
+  // unsigned bytes u = c + 8 straight from one mask (3 ALU ops per 8 codes instead of 7)
+  // and subtract 8 * sum(x) per (chunk, token, limb) in the epilogue; buckets with
+  // T >= 32 are epilogue-bound, so they convert to signed bytes in the unpack instead
+  // (measured: the correction cost T=64 draft 79 -> 89 us on 28672x8192).
+  static constexpr bool kUns = TMAX <= 16;
+  static constexpr int kALd = TMAX < 8 ? 8 : TMAX;  // ascale rows are a_ld = roundup(T, 8) <= kALd
+  // scale ring entry: [kCPS][128] weight scales | [kCPS][a_ld] activation scales | (kUns)
+  // [kCPS][a_ld][4] correction sums
+  static constexpr int kSEntry = kCPS * (128 + kALd + (kUns ? 4 * kALd : 0)) * 4;
+  static constexpr int kCorrOff = kCPS * (128 + kALd);  // floats
   static constexpr int kEpiThreads = kEpiWarps * 32;
   static constexpr int kTokChunk = TMAX < 8 ? TMAX : 8;  // tokens per epilogue token chunk (T <= 4 buckets: fewer)
   static constexpr int kOwnChunks = ((TMAX < 8 ? 8 : TMAX) / 8 + kEpiHalves - 1) / kEpiHalves;  // per epilogue warp
@@ -104,8 +120,18 @@ struct LinCfg {
   static constexpr int kSmemBytes = kBarOff + kNumBars * 8 + 16 + 4 * TMAX * 8 + 4 * 4 + 32 * 4 + 1024;
 };
 
-__device__ __forceinline__ uint32_t sext_nib(uint32_t n) {  // 4 nibbles (one per byte) -> 4 int8
-  return ((n ^ 0x88888888u) - 0x08080808u) ^ 0x80808080u;
+// 4 offset-binary nibbles (one per byte, u = c + 8) -> 4 int8 codes c = u - 8 (no borrow
+// crosses a byte: (u | 0x80) - 8 >= 0x78)
+__device__ __forceinline__ uint32_t ob_to_s8(uint32_t n) {
+  return ((n | 0x80808080u) - 0x08080808u) ^ 0x80808080u;
+}
+
+// Order register uses after an asynchronous TMEM load's tcgen05.wait::ld: an empty
+// volatile asm that "rewrites" each register (volatile asms keep their order).
+template <int N>
+__device__ __forceinline__ void reg_dep(uint32_t (&r)[N]) {
+#pragma unroll
+  for (int i = 0; i < N; ++i) asm volatile("" : "+r"(r[i]));
 }
 
 __device__ __forceinline__ long long umul_div(long long a, long long b, long long c) { return a * b / c; }
@@ -124,20 +150,31 @@ __device__ __forceinline__ float silu_ref(float g) {
   return __fdiv_rn(g, __fadd_rn(1.0f, expf(-g)));
 }
 
-// Stage iterator shared by every role: runs of <= CPS chunks of one tile.
+// Stage iterator shared by every role: runs of <= CPS chunks of one tile.  The (tile,
+// chunk) position advances incrementally -- one division at construction only (a
+// per-stage u / NC in every warp's loop showed up at ~10 % of the linear's samples).
 struct StageIt {
   int u, u1, NC, cps;
   int tile, ch0, nq;
+  int ntile, nch;  // position of u
+  __device__ __forceinline__ StageIt(int u0_, int u1_, int NC_, int cps_) : u(u0_), u1(u1_), NC(NC_), cps(cps_) {
+    ntile = u0_ / NC_;
+    nch = u0_ - ntile * NC_;
+  }
   __device__ __forceinline__ bool next() {
     if (u >= u1) return false;
-    tile = u / NC;
-    ch0 = u - tile * NC;
-    int end = u + cps;
-    const int tile_end = (tile + 1) * NC;
-    if (end > tile_end) end = tile_end;
-    if (end > u1) end = u1;
-    nq = end - u;
-    u = end;
+    tile = ntile;
+    ch0 = nch;
+    int n = NC - nch;
+    if (n > cps) n = cps;
+    if (n > u1 - u) n = u1 - u;
+    nq = n;
+    u += n;
+    nch += n;
+    if (nch == NC) {
+      nch = 0;
+      ++ntile;
+    }
     return true;
   }
 };
@@ -218,9 +255,13 @@ __global__ void __launch_bounds__(512, 1) linear_tc_kernel(const LinearArgs a) {
       int npro = 0;
       for (; npro < C::kStages && it.next(); ++npro) {
         uint8_t* st = smem + npro * C::kStageBytes;
-        mbar_arrive_expect_tx_elect(&wfull[npro], (uint32_t)it.nq * kChunkBytes);
-        bulk_g2s_elect(st, a.codes + ((size_t)it.tile * NC + it.ch0) * kChunkBytes, it.nq * kChunkBytes,
-                       &wfull[npro]);
+        if (QS_AB & 16) {
+          if (lane == 0) mbar_arrive(&wfull[npro]);
+        } else {
+          mbar_arrive_expect_tx_elect(&wfull[npro], (uint32_t)it.nq * kChunkBytes);
+          bulk_g2s_elect(st, a.codes + ((size_t)it.tile * NC + it.ch0) * kChunkBytes, it.nq * kChunkBytes,
+                         &wfull[npro]);
+        }
       }
       // L2 prefetch (no smem, no barrier): the rest of this CTA's own weight range, then
       // its share of the forward's look-ahead window (later linears' weights)
@@ -264,8 +305,13 @@ __global__ void __launch_bounds__(512, 1) linear_tc_kernel(const LinearArgs a) {
         const int s = i % C::kStages;
         mbar_wait(&empty[s], ((i / C::kStages) & 1) ^ 1);
         uint8_t* st = smem + s * C::kStageBytes;
-        mbar_arrive_expect_tx_elect(&wfull[s], (uint32_t)it.nq * kChunkBytes);
-        bulk_g2s_elect(st, a.codes + ((size_t)it.tile * NC + it.ch0) * kChunkBytes, it.nq * kChunkBytes, &wfull[s]);
+        if (QS_AB & 16) {
+          if (lane == 0) mbar_arrive(&wfull[s]);
+        } else {
+          mbar_arrive_expect_tx_elect(&wfull[s], (uint32_t)it.nq * kChunkBytes);
+          bulk_g2s_elect(st, a.codes + ((size_t)it.tile * NC + it.ch0) * kChunkBytes, it.nq * kChunkBytes,
+                         &wfull[s]);
+        }
         mbar_arrive_expect_tx_elect(&afull[s], (uint32_t)it.nq * act_bytes);
         bulk_g2s_elect(st + CPS * kChunkBytes, a.act + (size_t)it.ch0 * act_bytes, it.nq * act_bytes, &afull[s]);
         if (dbg0 && i < 64 && lane == 0) a.dbg[0 * 64 + i] = gtimer();
@@ -281,15 +327,17 @@ __global__ void __launch_bounds__(512, 1) linear_tc_kernel(const LinearArgs a) {
         const int ss = i % C::kSStages;
         mbar_wait(&sempty[ss], ((i / C::kSStages) & 1) ^ 1);
         float* se = sring + ss * (C::kSEntry / 4);
-        mbar_arrive_expect_tx_elect(&sfull[ss], (uint32_t)it.nq * (512u + a_bytes));
+        mbar_arrive_expect_tx_elect(&sfull[ss], (uint32_t)it.nq * (512u + (C::kUns ? 5u : 1u) * a_bytes));
         bulk_g2s_elect(se, a.wscale + ((size_t)it.tile * NC + it.ch0) * kTileN, it.nq * 512u, &sfull[ss]);
         bulk_g2s_elect(se + CPS * 128, a.ascale + (size_t)it.ch0 * a.a_ld, it.nq * a_bytes, &sfull[ss]);
+        if (C::kUns)
+          bulk_g2s_elect(se + C::kCorrOff, a.acorr + (size_t)it.ch0 * a.a_ld * 4, it.nq * 4u * a_bytes, &sfull[ss]);
       }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer (warp-wide, elected issue)
     {
-      const uint32_t idesc = idesc_i8(128, (uint32_t)a.r_pad);
+      const uint32_t idesc = idesc_i8(128, (uint32_t)a.r_pad, !C::kUns);
       StageIt it{u0, u1, NC, CPS};
       for (int i = 0; it.next(); ++i) {
         const int s = i % C::kStages, b = i % C::kAccBufs, as_ = i % C::kASlots;
@@ -308,7 +356,7 @@ __global__ void __launch_bounds__(512, 1) linear_tc_kernel(const LinearArgs a) {
         const uint32_t a0 = tmem + C::kAColBase + as_ * CPS * 32;
 #pragma unroll
         for (int q = 0; q < CPS; ++q)
-          if (q < it.nq)
+          if (!(QS_AB & 2) && q < it.nq)
             mma_i8_ts_chunk4_elect(d0 + q * C::kAccCols, a0 + q * 32,
                                    bdesc0 + (uint64_t)((q * C::kActBytes) >> 4), idesc);
         if (dbg0 && i < 64 && lane == 0) a.dbg[8 * 64 + i] = gtimer();
@@ -339,7 +387,7 @@ __global__ void __launch_bounds__(512, 1) linear_tc_kernel(const LinearArgs a) {
       uint4 wv[CPS][4];
 #pragma unroll
       for (int q = 0; q < kPre; ++q) {
-        if (q < it.nq) {
+        if (!(QS_AB & 1) && q < it.nq) {
           const uint4* src = reinterpret_cast<const uint4*>(smem + s * C::kStageBytes + q * kChunkBytes);
 #pragma unroll
           for (int jp = 0; jp < 4; ++jp) wv[q][jp] = src[jp * 128 + r];
@@ -348,23 +396,32 @@ __global__ void __launch_bounds__(512, 1) linear_tc_kernel(const LinearArgs a) {
 #pragma unroll
       for (int q = 0; q < CPS; ++q) {
         if (q < it.nq) {
-          if (q >= kPre) {
+          if (!(QS_AB & 1) && q >= kPre) {
             const uint4* src = reinterpret_cast<const uint4*>(smem + s * C::kStageBytes + q * kChunkBytes);
 #pragma unroll
             for (int jp = 0; jp < 4; ++jp) wv[q][jp] = src[jp * 128 + r];
           }
           uint32_t v[32];
+          if (QS_AB & 1) {
+#pragma unroll
+            for (int m = 0; m < 32; ++m) v[m] = (uint32_t)(r + m);
+          } else
 #pragma unroll
           for (int jp = 0; jp < 4; ++jp) {
             const uint32_t ww[4] = {wv[q][jp].x, wv[q][jp].y, wv[q][jp].z, wv[q][jp].w};
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               const int m = jp * 4 + e;
-              v[m] = sext_nib(ww[e] & 0x0F0F0F0Fu);
-              v[16 + m] = sext_nib((ww[e] >> 4) & 0x0F0F0F0Fu);
+              if constexpr (C::kUns) {
+                v[m] = ww[e] & 0x0F0F0F0Fu;
+                v[16 + m] = (ww[e] >> 4) & 0x0F0F0F0Fu;
+              } else {
+                v[m] = ob_to_s8(ww[e] & 0x0F0F0F0Fu);
+                v[16 + m] = ob_to_s8((ww[e] >> 4) & 0x0F0F0F0Fu);
+              }
             }
           }
-          tmem_st32(tmem + lane_base + C::kAColBase + (b * CPS + q) * 32, v);
+          if (!(QS_AB & 8)) tmem_st32(tmem + lane_base + C::kAColBase + (b * CPS + q) * 32, v);
         }
       }
       tmem_wait_st();
@@ -405,7 +462,11 @@ __global__ void __launch_bounds__(512, 1) linear_tc_kernel(const LinearArgs a) {
               uint32_t rr[8];
               tmem_ld8(col0 + c0, rr);
               tmem_wait_ld();
-              for (int e = 0; e < 8; ++e) a.dump[((size_t)n * NC + ch) * a.r_pad + c0 + e] = (int32_t)rr[e];
+              for (int e = 0; e < 8; ++e) {
+                const int col = c0 + e, tt = col / L, l = col - tt * L;
+                const int32_t corr = (C::kUns && tt < a.T) ? a.acorr[((size_t)ch * a.a_ld + tt) * 4 + l] : 0;
+                a.dump[((size_t)n * NC + ch) * a.r_pad + col] = (int32_t)rr[e] - corr;
+              }
             }
           }
         }
@@ -413,57 +474,76 @@ __global__ void __launch_bounds__(512, 1) linear_tc_kernel(const LinearArgs a) {
         float sw[CPS];
 #pragma unroll
         for (int q = 0; q < CPS; ++q) sw[q] = (q < it.nq) ? se[q * 128 + r] : 0.f;
+        // Software pipeline over this warp's token chunks: the TMEM loads of chunk lc+1
+        // are in flight while chunk lc's scale-accumulate runs (one tcgen05.ld -> wait
+        // round trip per token chunk was the 3-limb epilogue's critical path).  Only the
+        // columns of the chunk's tokens are drained (kCols = tokens x limbs).
+        constexpr int kCols = C::kTokChunk * L;
+        constexpr int KC = kCols <= 8 ? 8 : (kCols <= 16 ? 16 : 24);
+        // double-buffer only where the registers allow (no spills under the 128 cap)
+        constexpr bool kPipe = 2 * CPS * KC <= 64;
+        uint32_t rb[kPipe ? 2 : 1][CPS][KC];
+        auto issue = [&](int lc, uint32_t (&rr)[CPS][KC]) {
+#pragma unroll
+          for (int q = 0; q < CPS; ++q) {
+            if (q < it.nq) {
+              const uint32_t col0 = tmem + lane_base + (b * CPS + q) * C::kAccCols + (kH * lc + h) * 8 * L;
+              if constexpr (kCols <= 8) {
+                tmem_ld8(col0, *reinterpret_cast<uint32_t(*)[8]>(rr[q]));
+              } else if constexpr (kCols <= 16) {
+                tmem_ld16(col0, rr[q]);
+              } else {
+                tmem_ld16(col0, rr[q]);
+                tmem_ld8(col0 + 16, *reinterpret_cast<uint32_t(*)[8]>(rr[q] + 16));
+              }
+            }
+          }
+        };
+        const bool any = !(QS_AB & 4) && h * 8 < a.T;
+        if (any) issue(0, rb[0]);
 #pragma unroll
         for (int lc = 0; lc < kOwn; ++lc) {
           const int tc = kH * lc + h;
-          if (tc * 8 < a.T) {
-            // one TMEM round trip per token chunk for all chunks of the stage; only the
-            // columns of the chunk's tokens are drained (kCols = tokens x limbs)
-            constexpr int kCols = C::kTokChunk * L;
-            uint32_t rr[CPS][kCols <= 8 ? 8 : (kCols <= 16 ? 16 : 24)];
+          if (!any || tc * 8 >= a.T) break;
+          uint32_t(&rr)[CPS][KC] = rb[kPipe ? (lc & 1) : 0];
+          if (!kPipe && lc > 0) issue(lc, rr);
+          tmem_wait_ld();
 #pragma unroll
-            for (int q = 0; q < CPS; ++q) {
-              if (q < it.nq) {
-                const uint32_t col0 = tmem + lane_base + (b * CPS + q) * C::kAccCols + tc * 8 * L;
-                if constexpr (kCols <= 8) {
-                  tmem_ld8(col0, *reinterpret_cast<uint32_t(*)[8]>(rr[q]));
-                } else if constexpr (kCols <= 16) {
-                  tmem_ld16(col0, rr[q]);
-                } else {
-                  tmem_ld16(col0, rr[q]);
-                  tmem_ld8(col0 + 16, *reinterpret_cast<uint32_t(*)[8]>(rr[q] + 16));
-                }
-              }
-            }
-            tmem_wait_ld();
+          for (int q = 0; q < CPS; ++q) reg_dep(rr[q]);  // uses of rr stay after the wait
+          const bool more = lc + 1 < kOwn && (kH * (lc + 1) + h) * 8 < a.T;
+          if (more) {
+            if (kPipe) issue(lc + 1, rb[(lc + 1) & (kPipe ? 1 : 0)]);
+          } else {
             // every accumulator column this warp reads is in registers: hand the TMEM
             // buffer back to the MMA now, before the scale-accumulate math
-            if (lc == kOwn - 1 || (kH * (lc + 1) + h) * 8 >= a.T) {
-              tc_fence_before();
-              __syncwarp();
-              if (lane == 0) mbar_arrive(&accempty[b]);
-              released = true;
-            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&accempty[b]);
+            released = true;
+          }
 #pragma unroll
-            for (int q = 0; q < CPS; ++q) {
-              if (q < it.nq) {
-                const float* asc = se + CPS * 128 + q * a.a_ld;
-                const float4 s0 = *reinterpret_cast<const float4*>(asc + tc * 8);
-                const float4 s1 = *reinterpret_cast<const float4*>(asc + tc * 8 + 4);
-                const float as[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+          for (int q = 0; q < CPS; ++q) {
+            if (q < it.nq) {
+              const float* asc = se + CPS * 128 + q * a.a_ld;
+              const float4 s0 = *reinterpret_cast<const float4*>(asc + tc * 8);
+              const float4 s1 = *reinterpret_cast<const float4*>(asc + tc * 8 + 4);
+              const float as[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+              const int* corr = reinterpret_cast<const int*>(se + C::kCorrOff) + (q * a.a_ld + tc * 8) * 4;
 #pragma unroll
-                for (int e = 0; e < C::kTokChunk; ++e) {
-                  float dv;
-                  if constexpr (L == 1) {
-                    dv = (float)(int32_t)rr[q][e];
-                  } else {
-                    // token-major, limb-minor columns: X = l2*2^16 + l1*2^8 + l0.
-                    // d1*256+d0 is exact in int32; one rounding in the fma.
-                    const int32_t lo = (int32_t)rr[q][3 * e + 1] * 256 + (int32_t)rr[q][3 * e];
-                    dv = fmaf((float)(int32_t)rr[q][3 * e + 2], 65536.0f, (float)lo);
-                  }
-                  acc[lc * 8 + e] = fmaf(dv, sw[q] * as[e], acc[lc * 8 + e]);
+              for (int e = 0; e < C::kTokChunk; ++e) {
+                float dv;
+                // offset-binary correction (kUns): D = D' - 8 * S per limb
+                if constexpr (L == 1) {
+                  const int c0 = C::kUns ? corr[4 * e] : 0;
+                  dv = (float)((int32_t)rr[q][e] - c0);
+                } else {
+                  // token-major, limb-minor columns: X = l2*2^16 + l1*2^8 + l0.
+                  // d1*256+d0 is exact in int32; one rounding in the fma.
+                  const int2 cr = C::kUns ? *reinterpret_cast<const int2*>(corr + 4 * e + 2) : make_int2(0, 0);
+                  const int32_t lo = (int32_t)rr[q][3 * e + 1] * 256 + (int32_t)rr[q][3 * e] - cr.y;
+                  dv = fmaf((float)((int32_t)rr[q][3 * e + 2] - cr.x), 65536.0f, (float)lo);
                 }
+                acc[lc * 8 + e] = fmaf(dv, sw[q] * as[e], acc[lc * 8 + e]);
               }
             }
           }

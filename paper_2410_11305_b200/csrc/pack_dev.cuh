@@ -256,8 +256,9 @@ __device__ __forceinline__ void pack_group(const PackArgs& a, int t, int gi, flo
     const int o = it * 128 + lane * 4;
     if (!kLean && it * 128 >= a.gp) break;
     uint32_t w[L];
+    int lsum[L];  // this lane's part of the chunk's limb sums (offset-binary correction)
 #pragma unroll
-    for (int l = 0; l < L; ++l) w[l] = 0;
+    for (int l = 0; l < L; ++l) w[l] = 0, lsum[l] = 0;
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       int code[L];
@@ -283,7 +284,7 @@ __device__ __forceinline__ void pack_group(const PackArgs& a, int t, int gi, flo
         }
       }
 #pragma unroll
-      for (int l = 0; l < L; ++l) w[l] |= ((uint32_t)(code[l] & 0xFF)) << (8 * e);
+      for (int l = 0; l < L; ++l) w[l] |= ((uint32_t)(code[l] & 0xFF)) << (8 * e), lsum[l] += code[l];
     }
     if (a.img) {
       const int kp = gi * a.gp + o;
@@ -291,6 +292,14 @@ __device__ __forceinline__ void pack_group(const PackArgs& a, int t, int gi, flo
 #pragma unroll
       for (int l = 0; l < L; ++l)
         *reinterpret_cast<uint32_t*>(a.img + ch * chunk_stride + sw128_off(t * L + l, byte)) = w[l];
+      if (a.acorr) {
+        int S[3] = {0, 0, 0};
+#pragma unroll
+        for (int l = 0; l < L; ++l) S[l] = __reduce_add_sync(0xffffffffu, lsum[l]);
+        if (lane == 0)
+          *reinterpret_cast<int4*>(a.acorr + ((size_t)ch * a.a_ld + t) * 4) =
+              make_int4(8 * S[0], 8 * S[1], 8 * S[2], 8 * (256 * S[1] + S[0]));
+      }
     }
   }
 }

@@ -239,11 +239,11 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                : "memory");
 }
 
-// Instruction descriptor, kind::i8: D=S32, A=B=signed int8, both K-major.
-// Bit layout: cute::UMMA::InstrDescriptor (mma_sm100_desc.hpp).
-__host__ __device__ constexpr uint32_t idesc_i8(uint32_t m, uint32_t n) {
+// Instruction descriptor, kind::i8: D=S32, A = signed (a_signed) or unsigned int8,
+// B = signed int8, both K-major.  Bit layout: cute::UMMA::InstrDescriptor (mma_sm100_desc.hpp).
+__host__ __device__ constexpr uint32_t idesc_i8(uint32_t m, uint32_t n, bool a_signed = true) {
   return (2u << 4)            // c_format = S32
-         | (1u << 7)          // a_format = signed int8
+         | ((a_signed ? 1u : 0u) << 7)  // a_format: 1 = signed int8, 0 = unsigned
          | (1u << 10)         // b_format = signed int8
          | ((n >> 3) << 17)   // N >> 3
          | ((m >> 4) << 24);  // M >> 4

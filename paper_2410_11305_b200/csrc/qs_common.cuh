@@ -5,7 +5,9 @@
 //          tile  = 128 output rows, chunk = 128 (padded) K positions.
 //          piece j (0..3) of row r holds packed bytes pb = 16j..16j+15 of the
 //          row's 64-byte chunk; packed byte pb = nib(code[k=pb]) | nib(code[k=64+pb]) << 4
-//          (two's-complement nibbles, k relative to the chunk).  Groups of g
+//          with OFFSET-BINARY nibbles nib(c) = c + 8 (k relative to the chunk): one mask
+//          (and a shift) turns 4 nibbles into 4 unsigned bytes u = c + 8 for the tensor
+//          core, and sum_k c*x = sum_k u*x - 8 * sum_k x (the "acorr" sums below).  Groups of g
 //          codes are zero-padded to gp = roundup(g, 128) so every chunk belongs
 //          to exactly one quantisation group (cpg = gp/128 chunks per group).
 //   scales [n_tiles][n_chunks][128] fp32 (tile-major: one stage of a tile reads one
@@ -15,6 +17,9 @@
 //          row = token*L + limb.  L = 1 (W4A4 draft: int4 codes in int8),
 //          L = 3 (W4A16 verify: 24-bit fixed point split in three int8 limbs).
 //   ascale [n_chunks][a_ld] fp32 per (chunk, token): s_x (draft) or 2^-e (verify).
+//   acorr  [n_chunks][a_ld][4] int32 per (chunk, token), right after ascale in the same
+//          buffer: {8*S0, 8*S1, 8*S2, 8*(256*S1 + S0)}, S_l = sum over the chunk of the
+//          token's limb-l image bytes (L = 1: S0 only) -- the offset-binary correction.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -100,6 +105,7 @@ struct PackArgs {
   int T, K, g, gp, G, n_chunks, r_pad, a_ld;
   uint8_t* img;
   float* ascale;
+  int32_t* acorr;  // [n_chunks][a_ld][4] offset-binary correction sums (with img)
   int8_t* codes_out;
   float* scales_out;
   float* fq_out;
@@ -119,6 +125,7 @@ struct LinearArgs {
   const float* wscale;
   const uint8_t* act;
   const float* ascale;
+  const int32_t* acorr;  // [n_chunks][a_ld][4], see the layout notes above
   int n, n_pad, n_tiles, G, cpg, n_chunks;
   int T, r_pad, a_ld;
   int n_cta;

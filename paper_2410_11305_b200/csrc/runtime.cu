@@ -162,6 +162,7 @@ PackArgs pack_args(const qs_qweight_t& w, const float* x, int ldx, int T, const 
   p.a_ld = round_up(T, 8);
   p.img = ws->img;
   p.ascale = ws->ascale;
+  p.acorr = reinterpret_cast<int32_t*>(ws->ascale + (size_t)w.n_chunks * p.a_ld);
   return p;
 }
 
@@ -172,6 +173,7 @@ LinearArgs linear_args(const qs_qweight_t& w, int T, int L, const qs_workspace_t
   a.wscale = w.scales;
   a.act = ws->img;
   a.ascale = ws->ascale;
+  a.acorr = reinterpret_cast<const int32_t*>(ws->ascale + (size_t)w.n_chunks * round_up(T, 8));
   a.n = w.n;
   a.n_pad = w.n_pad;
   a.n_tiles = w.n_tiles;
@@ -368,7 +370,7 @@ int qs_workspace_size(const qs_model_t* m, int32_t t_max, qs_workspace_sizes_t* 
   out->attn = (size_t)t_max * m->d_model * 4;
   out->q = (size_t)t_max * m->n_heads * hd * 4;
   out->img = (size_t)chunks * img_rows(kMaxT, 3) * 128;
-  out->ascale = (size_t)chunks * kMaxT * 4;
+  out->ascale = (size_t)chunks * kMaxT * 4 * 5;  // ascale + acorr [n_chunks][a_ld][4]
   out->part = (size_t)(num_sms() + tiles) * kMaxT * kTileN * 4;
   out->counters = (size_t)(kGbarOffset + 2) * 4;
   if (tiles + 1 > kGbarOffset) return QS_ERR_SHAPE;

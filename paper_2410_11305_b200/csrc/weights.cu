@@ -79,14 +79,15 @@ __global__ void quantize_weight_kernel(const QuantWArgs a) {
     }
     int c = 0;
     if (s != 0.f) c = (int)fminf(fmaxf(rintf(__fdiv_rn(w, s)), -8.0f), 7.0f);
-    const uint32_t nib = (uint32_t)c & 0xFu;
+    const uint32_t nib = (uint32_t)c & 0xFu;     // reference nibble (two's complement)
+    const uint32_t dnib = nib ^ 0x8u;            // device nibble: offset binary, code + 8
     const int kp = gi * a.gp + o;
     const int ch = kp >> 7, kl = kp & 127;
     const int pb = kl & 63, hi = kl >> 6;
     const int piece = pb >> 4, b = pb & 15;
     uint8_t* dst = a.codes + ((((size_t)tile * a.n_chunks + ch) * 4 + piece) * kTileN + r) * 16 + b;
     // each (row, chunk) byte is owned by exactly this thread: plain RMW is safe
-    *dst = (uint8_t)(hi ? ((*dst & 0x0F) | (nib << 4)) : ((*dst & 0xF0) | nib));
+    *dst = (uint8_t)(hi ? ((*dst & 0x0F) | (dnib << 4)) : ((*dst & 0xF0) | dnib));
     if (a.ref_codes) {
       const long long fe = e0 + o;
       if (fe & 1) {
@@ -127,7 +128,7 @@ __global__ void repack_ref_kernel(const uint8_t* ref_codes, const float* ref_sca
   for (int o = 0; o < g; ++o) {
     const long long fe = (long long)n * cols + (long long)gi * g + o;
     const uint8_t byte = ref_codes[fe >> 1];
-    const uint32_t nib = (fe & 1) ? (byte >> 4) : (byte & 0xF);
+    const uint32_t nib = ((fe & 1) ? (byte >> 4) : (byte & 0xF)) ^ 0x8u;  // -> offset binary
     const int kp = gi * gp + o;
     const int ch = kp >> 7, kl = kp & 127;
     const int pb = kl & 63, hi = kl >> 6;

@@ -127,8 +127,9 @@ class DeviceStore:
         geo = self.geo
         raw = self.codes.cpu().numpy().reshape(geo.n_tiles, geo.n_chunks, 4, 128, 16)
         rows = raw.transpose(0, 3, 1, 2, 4).reshape(geo.n_pad, geo.n_chunks, 64)
-        lo = ((rows & 0x0F).astype(np.int8) ^ 8) - 8
-        hi = ((rows >> 4).astype(np.int8) ^ 8) - 8
+        # device nibbles are offset binary (code + 8; qs_common.cuh)
+        lo = (rows & 0x0F).astype(np.int8) - 8
+        hi = (rows >> 4).astype(np.int8) - 8
         full = np.concatenate([lo, hi], axis=2).reshape(geo.n_pad, geo.G, geo.gp)[:, :, :self.g]
         return full.reshape(geo.n_pad, self.k)[:self.n]
 
@@ -243,7 +244,7 @@ class _LinearWorkspace:
             chunks = (k // g) * gp // 128
             sms = _lib.i32()
             _lib.call("qs_num_sms", C_byref(sms))
-            sizes = dict(x=4, h=4, attn=4, q=4, img=chunks * 192 * 128, ascale=chunks * 64 * 4,
+            sizes = dict(x=4, h=4, attn=4, q=4, img=chunks * 192 * 128, ascale=chunks * 64 * 4 * 5,  # ascale + acorr
                          part=(sms.value + n_pad // 128) * 64 * 128 * 4, counters=(4096 + 2) * 4,
                          arg_val=(n_pad // 128) * 64 * 4, arg_idx=(n_pad // 128) * 64 * 4, att_o=4, att_ml=4)
             self.bufs = {kk: torch.zeros(v, dtype=torch.uint8, device="cuda") for kk, v in sizes.items()}
