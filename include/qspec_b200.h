@@ -147,6 +147,9 @@ int qs_linear_prepacked(const qs_qweight_t* w, int32_t T, int32_t mode, float* y
                         void* stream);
 /* debug: device buffer [6][256] u64 that qs_linear_prepacked fills with a CTA-0 %globaltimer timeline (NULL: off) */
 int qs_debug_timeline(uint64_t* buf);
+/* debug: the launch_index-th linear launch enqueued by qs_forward after this call (from 1;
+   0 = none) records that timeline (builds with -DQS_LIN_TIMELINE=1 only) */
+int qs_debug_select(int32_t launch_index);
 /* raw int32 per-(row, group, image-row) dots of the tensor-core integer core */
 int qs_linear_group_dots(const qs_qweight_t* w, const float* x, int32_t T, int32_t mode, int32_t* dots,
                          const qs_workspace_t* ws, void* stream);
@@ -179,6 +182,13 @@ int qs_forward(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const qs_
  * enqueued on `stream`), then added into the residual stream: one all-reduce per
  * block half, 2 per layer.  Returns the hook's failure as QS_ERR_CUDA. */
 typedef int (*qs_allreduce_fn)(float* ptr, int64_t count, void* stream, void* user);
+/* kernels the last qs_forward / qs_forward_tp call enqueued (host-side count) */
+int qs_forward_launches(void);
+/* fused next-operand emits, mask: 1 = gate_up's epilogue emits down_proj's operand, 2 = the
+   residual epilogues (o_proj, down_proj) emit the RMSNorm'd operand of the next linear;
+   0 = a separate act_pack before every linear.  Default: QS_EMIT env, else 3. */
+int qs_set_emit(int32_t mask);
+
 int qs_forward_tp(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const qs_workspace_t* ws, float* logits,
                   int32_t* argmax, int32_t world, qs_allreduce_fn allreduce, void* user, void* stream);
 

@@ -85,6 +85,9 @@ _SIGS = {
     "qs_w4a16_linear": ([C.POINTER(QWeight), vp, i32, vp, C.POINTER(Workspace), vp], C.c_int),
     "qs_linear_prepacked": ([C.POINTER(QWeight), i32, i32, vp, C.POINTER(Workspace), vp], C.c_int),
     "qs_debug_timeline": ([vp], C.c_int),
+    "qs_debug_select": ([i32], C.c_int),
+    "qs_forward_launches": ([], C.c_int),
+    "qs_set_emit": ([i32], C.c_int),
     "qs_linear_group_dots": ([C.POINTER(QWeight), vp, i32, i32, vp, C.POINTER(Workspace), vp], C.c_int),
     "qs_profile_enable": ([i32], C.c_int),
     "qs_profile_reset": ([], C.c_int),

@@ -89,7 +89,9 @@ struct LinCfg {
   static constexpr int kEpiWarps = 12 - kUnpackWarps;
   static constexpr int kEpiHalves = kEpiWarps / 4;
   static constexpr int kUnpackHalves = kUnpackWarps / 4;
-  static constexpr int kStages0 = (196 * 1024) / kStageBytes;
+  // residual-emit staging: the tile's new residual rows [T][128] + 1/rms per token
+  static constexpr int kStgBytes = (TMAX < 8 ? 8 : TMAX) * 129 * 4;
+  static constexpr int kStages0 = (196 * 1024 - kStgBytes) / kStageBytes;
   // Unpack group g takes the stages i with i % kUnpackHalves == g and waits on
   // wfull[i % kStages] by parity.  kStages must be a multiple of kUnpackHalves so
   // that each weight slot is only ever consumed by ONE group, which then observes
@@ -117,7 +119,9 @@ struct LinCfg {
   static constexpr int kScaleOff = kStages * kStageBytes;
   static constexpr int kBarOff = kScaleOff + kSStages * kSEntry;
   static constexpr int kNumBars = 3 * kStages + 2 * kASlots + 2 * kAccBufs + 2 * kSStages;
-  static constexpr int kSmemBytes = kBarOff + kNumBars * 8 + 16 + 4 * TMAX * 8 + 4 * 4 + 32 * 4 + 1024;
+  static constexpr int kStgOff = ((kBarOff + kNumBars * 8 + 16 + 4 * TMAX * 8 + 4 * 4 + 32 * 4) + 15) / 16 * 16;
+  static constexpr int kSmemBytes = kStgOff + kStgBytes + 1024;
+  static_assert(kSmemBytes <= 227 * 1024, "shared memory budget");
 };
 
 // 4 offset-binary nibbles (one per byte, u = c + 8) -> 4 int8 codes c = u - 8 (no borrow
@@ -188,6 +192,97 @@ __device__ __forceinline__ bool op_is(const LinearArgs& a) {
   if constexpr (!in_class) return false;
   if constexpr (OPC != kOpStore) return true;
   return a.op == O;
+}
+
+// ---------------------------------------------------------------- next-operand emits
+// kEmitRms (residual linears): stg = this tile's new residual rows [T][128] (+ [T] 1/rms
+// after them).  Leaf = tile: numpy's pairwise sum (numerics.py:60) over a 128 * 2^k row
+// splits down to 128-element leaves, each summed with 8 strided accumulators and the
+// ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) bracket; leaves combine as a balanced tree
+// (token_inv_rms in pack_dev.cuh states the same order).
+template <int L, int kEpiT, int kEpiWarps>
+__device__ __forceinline__ void emit_rms(const LinearArgs& a, float* stg, int tile, int et) {
+  const int lane = et & 31, ew = et >> 5;
+  named_bar(1, kEpiT);
+  for (int base = 0; base < a.T * 8; base += kEpiT) {
+    const int item = base + et, t = item >> 3, j = item & 7;
+    const bool on = t < a.T;
+    float rs = 0.f;
+    if (on) {
+      const float* xr = stg + t * 128;
+      rs = __fmul_rn(xr[j], xr[j]);
+#pragma unroll
+      for (int i = 1; i < 16; ++i) rs = __fadd_rn(rs, __fmul_rn(xr[8 * i + j], xr[8 * i + j]));
+    }
+    rs = __fadd_rn(rs, __shfl_xor_sync(0xffffffffu, rs, 1));
+    rs = __fadd_rn(rs, __shfl_xor_sync(0xffffffffu, rs, 2));
+    rs = __fadd_rn(rs, __shfl_xor_sync(0xffffffffu, rs, 4));
+    if (on && j == 0) __stcg(a.e_leaf + (size_t)t * a.n_tiles + tile, rs);
+  }
+  __threadfence();
+  named_bar(1, kEpiT);
+  if (et == 0) {
+    red_release_add(&a.e_cnt[0], 1);
+    const unsigned long long t0 = gtimer();
+    while (ld_acquire(&a.e_cnt[0]) < a.n_tiles) {
+      if (gtimer() - t0 > 5000000000ull) __trap();
+    }
+  }
+  named_bar(1, kEpiT);
+  float* inv = stg + 128 * (a.T > 8 ? a.T : 8);
+  const int nl = a.n_tiles, per = nl > 32 ? nl >> 5 : 1, lanes = nl > 32 ? 32 : nl;
+  for (int t = ew; t < a.T; t += kEpiWarps) {
+    const float* lf = a.e_leaf + (size_t)t * nl;
+    float s[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) s[i] = (i < per && lane * per + i < nl) ? __ldcg(lf + lane * per + i) : 0.f;
+    if (per >= 2) s[0] = __fadd_rn(s[0], s[1]);
+    if (per >= 4) {
+      s[2] = __fadd_rn(s[2], s[3]);
+      s[0] = __fadd_rn(s[0], s[2]);
+    }
+    float v = s[0];
+    for (int off = 1; off < lanes; off <<= 1) v = __fadd_rn(v, __shfl_xor_sync(0xffffffffu, v, off));
+    if (lane == 0) {
+      const float ms = __fdiv_rn(v, (float)a.e_n);
+      inv[t] = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(ms, a.e_eps)));
+    }
+  }
+  named_bar(1, kEpiT);
+  if (et == 0) {  // the last owner through resets both counters (every owner is past the wait)
+    if (atomicAdd(&a.e_cnt[1], 1) == a.n_tiles - 1) {
+      a.e_cnt[0] = 0;
+      a.e_cnt[1] = 0;
+    }
+  }
+  for (int t = ew; t < a.T; t += kEpiWarps) {
+    const float iv = inv[t];
+    const float4 xv = *reinterpret_cast<const float4*>(stg + t * 128 + 4 * lane);
+    const float4 wv = *reinterpret_cast<const float4*>(a.e_rms_w + (size_t)tile * 128 + 4 * lane);
+    const float v[4] = {__fmul_rn(__fmul_rn(xv.x, iv), wv.x), __fmul_rn(__fmul_rn(xv.y, iv), wv.y),
+                        __fmul_rn(__fmul_rn(xv.z, iv), wv.z), __fmul_rn(__fmul_rn(xv.w, iv), wv.w)};
+    quant_group_warp<L>(v, t, tile, lane, a.e_img, a.e_ascale, a.e_acorr, a.r_pad, a.a_ld);
+  }
+}
+
+// kEmitSilu (gate_up): tiles 2q, 2q+1 hold silu outputs 128q..128q+127 = group q of
+// down_proj's input.  Each owner publishes its half; the second one quantises the group.
+template <int L, int kEpiT, int kEpiWarps>
+__device__ __forceinline__ void emit_silu(const LinearArgs& a, int tile, int et, int* flag) {
+  const int lane = et & 31, ew = et >> 5, q = tile >> 1;
+  __threadfence();
+  named_bar(1, kEpiT);
+  if (et == 0) *flag = atom_add_acq_rel(&a.e_cnt[8 + q], 1);
+  named_bar(1, kEpiT);
+  const int second = *flag;
+  named_bar(1, kEpiT);
+  if (second != 1) return;
+  for (int t = ew; t < a.T; t += kEpiWarps) {
+    const float4 hv = __ldcg(reinterpret_cast<const float4*>(a.out + (size_t)t * a.ldo + 128 * q) + lane);
+    const float v[4] = {hv.x, hv.y, hv.z, hv.w};
+    quant_group_warp<L>(v, t, q, lane, a.e_img, a.e_ascale, a.e_acorr, a.r_pad, a.a_ld);
+  }
+  if (et == 0) a.e_cnt[8 + q] = 0;
 }
 
 template <int L, int TMAX, int OPC>
@@ -294,6 +389,7 @@ __global__ void __launch_bounds__(512, 1) linear_tc_kernel(const LinearArgs a) {
       }
       __syncwarp();
       pdl_wait();
+      if (QS_LIN_TIMELINE && a.dbg && lane == 0) a.dbg[4096 + c] = gtimer();
       StageIt ia{u0, u1, NC, CPS};
       for (int i = 0; i < npro && ia.next(); ++i) {
         uint8_t* st = smem + i * C::kStageBytes;
@@ -319,19 +415,34 @@ __global__ void __launch_bounds__(512, 1) linear_tc_kernel(const LinearArgs a) {
     }
   } else if (warp == 3) {
     // ------------------------------------------------------------ scale producer (warp-wide, elected issue)
+    // Weight scales do not depend on the previous kernel: the first kSStages entries'
+    // weight scales are requested before griddepcontrol.wait (with the whole entry's
+    // byte count expected up front), the activation scales / correction sums after it.
     {
-      pdl_wait();
       const uint32_t a_bytes = (uint32_t)a.a_ld * 4u;
+      const uint32_t e_bytes = 512u + (C::kUns ? 5u : 1u) * a_bytes;  // per chunk
+      auto act_part = [&](float* se, const StageIt& st, int ss) {
+        bulk_g2s_elect(se + CPS * 128, a.ascale + (size_t)st.ch0 * a.a_ld, st.nq * a_bytes, &sfull[ss]);
+        if (C::kUns)
+          bulk_g2s_elect(se + C::kCorrOff, a.acorr + (size_t)st.ch0 * a.a_ld * 4, st.nq * 4u * a_bytes, &sfull[ss]);
+      };
       StageIt it{u0, u1, NC, CPS};
-      for (int i = 0; it.next(); ++i) {
+      int npro = 0;
+      for (; npro < C::kSStages && it.next(); ++npro) {
+        float* se = sring + npro * (C::kSEntry / 4);
+        mbar_arrive_expect_tx_elect(&sfull[npro], (uint32_t)it.nq * e_bytes);
+        bulk_g2s_elect(se, a.wscale + ((size_t)it.tile * NC + it.ch0) * kTileN, it.nq * 512u, &sfull[npro]);
+      }
+      pdl_wait();
+      StageIt ia{u0, u1, NC, CPS};
+      for (int i = 0; i < npro && ia.next(); ++i) act_part(sring + i * (C::kSEntry / 4), ia, i);
+      for (int i = npro; it.next(); ++i) {
         const int ss = i % C::kSStages;
         mbar_wait(&sempty[ss], ((i / C::kSStages) & 1) ^ 1);
         float* se = sring + ss * (C::kSEntry / 4);
-        mbar_arrive_expect_tx_elect(&sfull[ss], (uint32_t)it.nq * (512u + (C::kUns ? 5u : 1u) * a_bytes));
+        mbar_arrive_expect_tx_elect(&sfull[ss], (uint32_t)it.nq * e_bytes);
         bulk_g2s_elect(se, a.wscale + ((size_t)it.tile * NC + it.ch0) * kTileN, it.nq * 512u, &sfull[ss]);
-        bulk_g2s_elect(se + CPS * 128, a.ascale + (size_t)it.ch0 * a.a_ld, it.nq * a_bytes, &sfull[ss]);
-        if (C::kUns)
-          bulk_g2s_elect(se + C::kCorrOff, a.acorr + (size_t)it.ch0 * a.a_ld * 4, it.nq * 4u * a_bytes, &sfull[ss]);
+        act_part(se, it, ss);
       }
     }
   } else if (warp == 1) {
@@ -345,6 +456,7 @@ __global__ void __launch_bounds__(512, 1) linear_tc_kernel(const LinearArgs a) {
         mbar_wait(&accempty[b], ((i / C::kAccBufs) & 1) ^ 1);
         if (dbg0 && i < 64 && lane == 0) a.dbg[5 * 64 + i] = gtimer();
         mbar_wait(&afull[s], (i / C::kStages) & 1);
+        if (QS_LIN_TIMELINE && a.dbg && i == 0 && lane == 0) a.dbg[4608 + c] = gtimer();
         if (dbg0 && i < 64 && lane == 0) a.dbg[6 * 64 + i] = gtimer();
         mbar_wait(&tfull[as_], (i / C::kASlots) & 1);
         tc_fence_after();
@@ -592,6 +704,7 @@ __global__ void __launch_bounds__(512, 1) linear_tc_kernel(const LinearArgs a) {
             if (gtimer() - t0 > 5000000000ull) __trap();
           }
           a.counters[tile] = 0;
+          if (QS_LIN_TIMELINE && a.dbg) a.dbg[5120 + c] = gtimer();
         }
         named_bar(1, kEpiT);
         constexpr int kPB = kOwn <= 1 ? 4 : (kOwn == 2 ? 2 : 1);
@@ -626,7 +739,9 @@ __global__ void __launch_bounds__(512, 1) linear_tc_kernel(const LinearArgs a) {
           if (op_is<OPC, kOpStore>(a) || op_is<OPC, kOpResidual>(a)) {
             if (t < a.T && valid) {
               float* o = a.out + (size_t)t * a.ldo + n;
-              *o = (op_is<OPC, kOpResidual>(a)) ? __fadd_rn(*o, v) : v;
+              const float nv = (op_is<OPC, kOpResidual>(a)) ? __fadd_rn(*o, v) : v;
+              *o = nv;
+              if (OPC == kOpStore && a.emit == kEmitRms) reinterpret_cast<float*>(smem + C::kStgOff)[t * 128 + r] = nv;
             }
           } else if (op_is<OPC, kOpSiluMul>(a)) {
             const float other = __shfl_xor_sync(0xffffffffu, v, 1);
@@ -712,10 +827,16 @@ __global__ void __launch_bounds__(512, 1) linear_tc_kernel(const LinearArgs a) {
           if (et == 0) a.counters[a.n_tiles] = 0;
         }
       }
+      if constexpr (OPC == kOpStore) {
+        if (a.emit == kEmitRms) emit_rms<L, kEpiT, C::kEpiWarps>(a, reinterpret_cast<float*>(smem + C::kStgOff), tile, et);
+      } else if constexpr (OPC == kOpSiluMul) {
+        if (a.emit == kEmitSilu) emit_silu<L, kEpiT, C::kEpiWarps>(a, tile, et, flag);
+      }
 #pragma unroll
       for (int t = 0; t < kOwn * 8; ++t) acc[t] = 0.f;
     }
   }
+  if (QS_LIN_TIMELINE && a.dbg && warp == 4 + C::kUnpackWarps && lane == 0) a.dbg[5632 + c] = gtimer();
   tc_fence_before();
   __syncthreads();
   if (warp == 2) {

@@ -182,6 +182,71 @@ __device__ __forceinline__ float token_inv_rms(const PackArgs& a, int t, int tid
   return __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(ms, a.eps)));
 }
 
+// One warp quantises one 128-element group of token t (lane holds elements 4*lane..+3,
+// already normalised) into chunk `ch` of the operand image + its activation scale and
+// offset-binary correction sums -- the same arithmetic as pack_group's plain path (the
+// linear epilogues use it to emit the NEXT linear's operand; tests check the fused and
+// the act_pack operands are bit-identical).
+template <int L>
+__device__ __forceinline__ void quant_group_warp(const float (&v)[4], int t, int ch, int lane, uint8_t* img,
+                                                 float* ascale, int32_t* acorr, int r_pad, int a_ld) {
+  float m = fmaxf(fmaxf(fabsf(v[0]), fabsf(v[1])), fmaxf(fabsf(v[2]), fabsf(v[3])));
+  m = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(m)));
+  float s, mul;
+  int e2 = 0;
+  if constexpr (L == 1) {
+    m = snap_group_max(m);
+    s = __fdiv_rn(m, 7.0f);
+    mul = s;
+  } else {
+    if (m > 0.f) {
+      int E;
+      frexpf(m, &E);
+      e2 = 22 - E;
+      mul = ldexpf(1.0f, -e2);
+    } else {
+      mul = 0.f;
+    }
+    s = mul;
+  }
+  uint32_t w[L];
+  int lsum[L];
+#pragma unroll
+  for (int l = 0; l < L; ++l) w[l] = 0, lsum[l] = 0;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    int code[L];
+    const float x = v[e];
+    if constexpr (L == 1) {
+      float qv = 0.f;
+      if (s != 0.f) qv = fminf(fmaxf(rintf(__fdiv_rn(x, s)), -8.0f), 7.0f);
+      code[0] = (int)qv;
+    } else {
+      const int X = (m > 0.f) ? __float2int_rn(ldexpf(x, e2)) : 0;
+      const int l0 = ((X + 128) & 255) - 128;
+      const int X1 = (X - l0) >> 8;
+      const int l1 = ((X1 + 128) & 255) - 128;
+      code[0] = l0;
+      code[1 % L] = l1;
+      code[2 % L] = (X1 - l1) >> 8;
+    }
+#pragma unroll
+    for (int l = 0; l < L; ++l) w[l] |= ((uint32_t)(code[l] & 0xFF)) << (8 * e), lsum[l] += code[l];
+  }
+  const size_t chunk_stride = (size_t)r_pad * 128;
+#pragma unroll
+  for (int l = 0; l < L; ++l)
+    *reinterpret_cast<uint32_t*>(img + ch * chunk_stride + sw128_off(t * L + l, lane * 4)) = w[l];
+  int S[3] = {0, 0, 0};
+#pragma unroll
+  for (int l = 0; l < L; ++l) S[l] = __reduce_add_sync(0xffffffffu, lsum[l]);
+  if (lane == 0) {
+    ascale[(size_t)ch * a_ld + t] = mul;
+    *reinterpret_cast<int4*>(acorr + ((size_t)ch * a_ld + t) * 4) =
+        make_int4(8 * S[0], 8 * S[1], 8 * S[2], 8 * (256 * S[1] + S[0]));
+  }
+}
+
 // One warp quantises group gi of token t into the operand image (+ scales).
 // kPlain: the common operand (no attention combine, g % 4 == 0, gp == 128) -- one
 // float4 per lane and none of the general paths, so the kernel's code stays small

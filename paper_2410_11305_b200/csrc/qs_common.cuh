@@ -85,6 +85,8 @@ struct KTraceScope {
   __device__ __forceinline__ ~KTraceScope() { ktrace_exit(k); }
 };
 
+enum Emit : int { kEmitNone = 0, kEmitSilu = 1, kEmitRms = 2 };
+
 enum PostOp : int {
   kOpStore = 0,     // out[t, n] = y
   kOpResidual = 1,  // out[t, n] += y          (o_proj / down_proj)
@@ -162,6 +164,22 @@ struct LinearArgs {
   int pf_n;
   int pf_own;
   KTrace kt;
+  // Next-operand emit: the act pack of the NEXT linear fused into this epilogue.
+  //   kEmitSilu (gate_up): the owner that completes a 128-wide group of silu outputs (a
+  //     pair of interleaved gate/up tiles) quantises it into down_proj's operand chunk.
+  //   kEmitRms (o_proj / down_proj residual): every tile owner publishes its numpy
+  //     pairwise leaf sum of squares (leaf = tile = 128 elements), waits for all owners,
+  //     forms 1/rms per token exactly as numerics.py:46-62 and quantises its own tile --
+  //     one group -- of the RMSNorm'd row into the next linear's operand chunk.
+  int emit;
+  uint8_t* e_img;
+  float* e_ascale;
+  int32_t* e_acorr;
+  const float* e_rms_w;
+  float e_eps;
+  int e_n;         // row width (the RMSNorm mean's n)
+  float* e_leaf;   // [T][n_tiles]
+  int* e_cnt;      // [0] arrive, [1] depart (kEmitRms); [8 + q] per group (kEmitSilu); zero on entry and exit
   // debug timeline (CTA 0): [role][i] globaltimer ns; roles: 0 producer issue, 1 unpack done,
   // 2 mma issued, 3 epilogue start (acc ready), 4 epilogue done
   unsigned long long* dbg;

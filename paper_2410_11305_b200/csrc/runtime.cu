@@ -60,6 +60,7 @@ bool pdl_enabled() {
 }  // namespace qs
 
 static unsigned long long* g_dbg = nullptr;
+static int g_dbg_want = 0, g_dbg_seen = 0;
 namespace {
 
 // qs_ktrace_*: per-launch slots of the device timeline (KTrace in qs_common.cuh)
@@ -76,7 +77,8 @@ KTrace next_trace(int32_t tag) {
 }
 
 constexpr int kMaxT = 64;
-constexpr int kGbarOffset = 4096;  // grid-barrier words live past every per-tile counter
+constexpr int kGbarOffset = 4096;  // emit counters live past every per-tile counter
+constexpr int kEmitCnt = 8 + 1024;  // [0] arrive, [1] depart, [8 + q] per silu group
 
 int g_num_sms = 0;
 
@@ -116,14 +118,24 @@ namespace {
 
 // Launch a linear whose operand comes from a.pk: a separate act_pack launch
 // overlapped via PDL, then the linear.
-cudaError_t launch_linear_packed(int L, LinearArgs& a, cudaStream_t st, int32_t tag = -1) {
+int g_launches = 0;  // kernels enqueued by the last qs_forward (qs_forward_launches)
+
+cudaError_t launch_linear_packed(int L, LinearArgs& a, cudaStream_t st, int32_t tag = -1, bool pack = true) {
   const int32_t mode_bits = 16 * (L == 1 ? 1 : 0);
-  prof_mark(st, mode_bits + 5, true);  // kind 5: operand pack
-  a.pk.kt = next_trace(mode_bits + 5);
-  cudaError_t e = launch_act_pack(L, a.pk, st);
-  prof_mark(st, 0, false);
-  if (e != cudaSuccess) return e;
+  cudaError_t e = cudaSuccess;
+  if (pack) {  // else the operand was emitted by the previous linear's epilogue
+    prof_mark(st, mode_bits + 5, true);  // kind 5: operand pack
+    a.pk.kt = next_trace(mode_bits + 5);
+    e = launch_act_pack(L, a.pk, st);
+    prof_mark(st, 0, false);
+    if (e != cudaSuccess) return e;
+    ++g_launches;
+  }
+  ++g_launches;
   a.kt = next_trace(tag >= 0 ? tag : mode_bits + 15);
+  // qs_debug_select(j): the j-th linear launch enqueued after the call records its CTA
+  // timeline into the qs_debug_timeline buffer (QS_LIN_TIMELINE builds only)
+  if (g_dbg_want > 0 && ++g_dbg_seen == g_dbg_want) a.dbg = g_dbg;
   if (tag >= 0) prof_mark(st, tag, true);
   e = launch_linear(L, a, st);
   if (tag >= 0) prof_mark(st, 0, false);
@@ -369,10 +381,11 @@ int qs_workspace_size(const qs_model_t* m, int32_t t_max, qs_workspace_sizes_t* 
   out->h = (size_t)t_max * m->d_ff * 4;
   out->attn = (size_t)t_max * m->d_model * 4;
   out->q = (size_t)t_max * m->n_heads * hd * 4;
-  out->img = (size_t)chunks * img_rows(kMaxT, 3) * 128;
-  out->ascale = (size_t)chunks * kMaxT * 4 * 5;  // ascale + acorr [n_chunks][a_ld][4]
+  out->img = 2 * (size_t)chunks * img_rows(kMaxT, 3) * 128;  // two operand slots (emit double buffer)
+  out->ascale = 2 * (size_t)chunks * kMaxT * 4 * 5;  // two slots of ascale + acorr [n_chunks][a_ld][4]
   out->part = (size_t)(num_sms() + tiles) * kMaxT * kTileN * 4;
-  out->counters = (size_t)(kGbarOffset + 2) * 4;
+  // per-tile counters | emit counters [kGbarOffset, +8 + 1024) | emit leaf sums [kMaxT][<=128]
+  out->counters = (size_t)(kGbarOffset + kEmitCnt + kMaxT * 128) * 4;
   if (tiles + 1 > kGbarOffset) return QS_ERR_SHAPE;
   out->arg_val = (size_t)wl.n_tiles * kMaxT * 4;
   out->arg_idx = (size_t)wl.n_tiles * kMaxT * 4;
@@ -500,6 +513,12 @@ int qs_debug_timeline(uint64_t* buf) {
   return QS_OK;
 }
 
+int qs_debug_select(int32_t launch_index) {
+  g_dbg_want = launch_index;
+  g_dbg_seen = 0;
+  return QS_OK;
+}
+
 int qs_linear_prepacked(const qs_qweight_t* w, int32_t T, int32_t mode, float* y, const qs_workspace_t* ws,
                         void* stream) {
   int rc = check_weight(w);
@@ -524,6 +543,39 @@ struct TpHooks {
   qs_allreduce_fn fn;
   void* user;
 };
+// Operand slots: the image + scales a linear reads, and the one its epilogue emits for
+// the NEXT linear, must differ (some CTAs still stream their operand while finished
+// owners emit), so the workspace holds two and the forward alternates between them.
+struct Slot {
+  uint8_t* img;
+  float* ascale;
+};
+void use_slot(LinearArgs& a, const qs_qweight_t& w, const Slot& sl) {
+  a.act = sl.img;
+  a.ascale = sl.ascale;
+  a.acorr = reinterpret_cast<const int32_t*>(sl.ascale + (size_t)w.n_chunks * a.a_ld);
+  a.pk.img = sl.img;
+  a.pk.ascale = sl.ascale;
+  a.pk.acorr = reinterpret_cast<int32_t*>(sl.ascale + (size_t)w.n_chunks * a.pk.a_ld);
+}
+void set_emit(LinearArgs& a, int kind, const qs_qweight_t& next, const Slot& sl, const float* rms_w, float eps,
+              int n, const qs_workspace_t* ws) {
+  a.emit = kind;
+  a.e_img = sl.img;
+  a.e_ascale = sl.ascale;
+  a.e_acorr = reinterpret_cast<int32_t*>(sl.ascale + (size_t)next.n_chunks * a.a_ld);
+  a.e_rms_w = rms_w;
+  a.e_eps = eps;
+  a.e_n = n;
+  a.e_cnt = ws->counters + kGbarOffset;
+  a.e_leaf = reinterpret_cast<float*>(ws->counters + kGbarOffset + kEmitCnt);
+}
+int g_emit = -1;  // fused next-operand emits (mask: 1 silu, 2 rmsnorm): -1 = QS_EMIT env (default 3)
+int emit_mask() {
+  if (g_emit < 0) g_emit = env_int("QS_EMIT", 3) & 3;
+  return g_emit;
+}
+
 int forward_impl(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const qs_workspace_t* ws, float* logits,
                  int32_t* argmax, cudaStream_t st, const TpHooks* tp) {
   const int T = b->T;
@@ -531,6 +583,7 @@ int forward_impl(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const q
   const int L = mode == QS_MODE_LOW ? 1 : 3;
   const int world = tp ? tp->world : 1;
   const int d = m->d_model, H = m->n_heads, KV = m->n_kv_heads, hd = d / (H * world), ff = m->d_ff;
+  g_launches = 0;
   // tensor parallel: o_proj / down_proj are row-split, so their outputs are partial
   // sums -> store into ws->attn, all-reduce (caller's hook, e.g. NCCL on this
   // stream), then add into the residual stream
@@ -539,6 +592,7 @@ int forward_impl(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const q
   auto reduce_into_x = [&]() -> int {
     int rc = tp->fn(ws->attn, (int64_t)T * d, st, tp->user);
     if (rc != 0) return QS_ERR_CUDA;
+    ++g_launches;
     return status(launch_add_rows(ws->x, ws->attn, T * d, st));
   };
   const int hpk = H / KV;
@@ -546,6 +600,31 @@ int forward_impl(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const q
   if (b->ctx_cap > m->rope_len) return QS_ERR_OVERFLOW;
   const int att_cmax = attention_chunks(m->rope_len);
   if (attention_smem_bytes(b->blk_qmax, hpk, hd, b->ctx_cap) > 200 * 1024) return QS_ERR_SHAPE;
+  // operand slots (qs_workspace_size allots two)
+  Slot slot[2];
+  {
+    qs_qweight_t wd, wf;
+    fill_geometry(d, d, m->group_size, &wd);
+    fill_geometry(d, ff, m->group_size, &wf);
+    const int chunks = wd.n_chunks > wf.n_chunks ? wd.n_chunks : wf.n_chunks;
+    slot[0] = Slot{ws->img, ws->ascale};
+    slot[1] = Slot{ws->img + (size_t)chunks * img_rows(kMaxT, 3) * 128, ws->ascale + (size_t)chunks * kMaxT * 5};
+  }
+  // fused next-operand emits (LinearArgs::emit): not under TP (the residual is added after
+  // the all-reduce), g = 128 only (a tile is a group), d = 128 * 2^k (a tile is a numpy
+  // pairwise leaf) and every CTA owning at most one residual tile
+  // Measured (bench.py, B=1 / B=16): the emits win for small forwards (AR 2.38 -> 2.33 ms)
+  // and lose at T=64 (the 32 o/down owners quantise 64 tokens each while the act_pack
+  // kernel spreads them over 512 CTAs and overlaps the next linear's weight prefetch), so
+  // they run for T <= QS_EMIT_TMAX (default 16) only.
+  static const int emit_tmax = env_int("QS_EMIT_TMAX", 16);
+  const bool emit_ok = !tp && T <= emit_tmax && m->group_size == 128 && d % 128 == 0;
+  const int d_tiles = d / 128;
+  // (o_proj / down_proj have d/128 tiles of >= d/128 chunks: n_cta = min(units, #SMs) >= n_tiles
+  // iff n_tiles <= #SMs, and then no CTA's unit range holds two tile starts)
+  const bool emit_rms =
+      emit_ok && (emit_mask() & 2) && (d_tiles & (d_tiles - 1)) == 0 && d_tiles <= 128 && d_tiles <= num_sms();
+  const bool emit_silu = emit_ok && (emit_mask() & 1) && ff % 128 == 0 && ff / 128 <= kEmitCnt - 8;
   cudaError_t e;
   WeightStream ws_stream;
   for (int li = 0; li < m->n_layers; ++li) {
@@ -556,6 +635,8 @@ int forward_impl(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const q
   }
   ws_stream.add_linear(m->lm_head);
   int lin_j = 0;
+  const int s0 = 0;            // slot read by qkv / gate_up / lm_head
+  bool qkv_ready = false;      // qkv's operand already emitted by the previous down_proj
   for (int li = 0; li < m->n_layers; ++li) {
     const qs_layer_t& ly = m->layers[li];
     // q|k|v projection; operand = rmsnorm(x) (+ embedding gather on layer 0), fused
@@ -569,6 +650,7 @@ int forward_impl(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const q
       a.pk.emb = m->tok_emb;
       a.pk.x_out = ws->x;
     }
+    use_slot(a, ly.qkv, slot[s0]);
     a.pos = b->positions;
     a.slot = b->slots;
     a.rope_cos = m->rope_cos;
@@ -583,7 +665,7 @@ int forward_impl(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const q
     a.bt_ld = m->bt_ld;
     a.page = m->page;
     ws_stream.window(a, lin_j++);
-    if ((e = launch_linear_packed(L, a, st, mode * 16 + 0)) != cudaSuccess) return status(e);
+    if ((e = launch_linear_packed(L, a, st, mode * 16 + 0, !qkv_ready)) != cudaSuccess) return status(e);
     // attention (model.py:293-330), split-KV partials
     AttnArgs at{};
     at.q = ws->q;
@@ -612,8 +694,10 @@ int forward_impl(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const q
     prof_mark(st, mode * 16 + 6, true);  // kind 6: attention
     at.kt = next_trace(mode * 16 + 6);
     if ((e = launch_attention(at, b->n_blk, st)) != cudaSuccess) return status(e);
+    ++g_launches;
     prof_mark(st, 0, false);
-    // o_proj + residual (model.py:332); its fused pre-phase merges the attention chunks
+    // o_proj + residual (model.py:332); its operand pack merges the attention chunks;
+    // its epilogue emits gate_up's operand rmsnorm(x) * ffn_norm (model.py:333)
     a = linear_args(ly.o, T, L, ws, res_op, res_out, d);
     a.pk = pack_args(ly.o, ws->attn, ly.o.k, T, ws, L);
     a.pk.att_o = ws->att_o;
@@ -622,37 +706,50 @@ int forward_impl(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const q
     a.pk.att_hd = hd;
     a.pk.att_cmax = att_cmax;
     a.pk.att_chunk = attention_chunk_len();
+    use_slot(a, ly.o, slot[s0 ^ 1]);
+    if (emit_rms) set_emit(a, kEmitRms, ly.gate_up, slot[s0], ly.ffn_norm, m->norm_eps, d, ws);
     ws_stream.window(a, lin_j++);
     if ((e = launch_linear_packed(L, a, st, mode * 16 + 1)) != cudaSuccess) return status(e);
     if (tp) {
       const int rc = reduce_into_x();
       if (rc) return rc;
     }
-    // gate|up on rmsnorm(x), epilogue silu(gate) * up (model.py:333-335)
+    // gate|up on rmsnorm(x), epilogue silu(gate) * up (model.py:333-335), then down_proj's
+    // operand groups
     a = linear_args(ly.gate_up, T, L, ws, kOpSiluMul, ws->h, ff);
     a.pk = pack_args(ly.gate_up, ws->x, d, T, ws, L);
     a.pk.rms_w = ly.ffn_norm;
     a.pk.eps = m->norm_eps;
+    use_slot(a, ly.gate_up, slot[s0]);
+    if (emit_silu) set_emit(a, kEmitSilu, ly.down, slot[s0 ^ 1], nullptr, 0.f, ff, ws);
     ws_stream.window(a, lin_j++);
-    if ((e = launch_linear_packed(L, a, st, mode * 16 + 2)) != cudaSuccess) return status(e);
-    // down_proj + residual (model.py:336)
+    if ((e = launch_linear_packed(L, a, st, mode * 16 + 2, !emit_rms)) != cudaSuccess) return status(e);
+    // down_proj + residual (model.py:336); epilogue emits the next qkv's (or lm_head's)
+    // operand rmsnorm(x) * attn_norm / final_norm (model.py:302, 342)
     a = linear_args(ly.down, T, L, ws, res_op, res_out, d);
     a.pk = pack_args(ly.down, ws->h, ff, T, ws, L);
+    use_slot(a, ly.down, slot[s0 ^ 1]);
+    const bool last = li + 1 == m->n_layers;
+    if (emit_rms)
+      set_emit(a, kEmitRms, last ? m->lm_head : m->layers[li + 1].qkv, slot[s0],
+               last ? m->final_norm : m->layers[li + 1].attn_norm, m->norm_eps, d, ws);
     ws_stream.window(a, lin_j++);
-    if ((e = launch_linear_packed(L, a, st, mode * 16 + 3)) != cudaSuccess) return status(e);
+    if ((e = launch_linear_packed(L, a, st, mode * 16 + 3, !emit_silu)) != cudaSuccess) return status(e);
     if (tp) {
       const int rc = reduce_into_x();
       if (rc) return rc;
     }
+    qkv_ready = emit_rms;
   }
   // final norm + lm_head + argmax (model.py:342-344, numerics.py:81-86)
   LinearArgs a = linear_args(m->lm_head, T, L, ws, kOpLogits, logits, m->vocab);
   a.pk = pack_args(m->lm_head, ws->x, d, T, ws, L);
   a.pk.rms_w = m->final_norm;
   a.pk.eps = m->norm_eps;
+  use_slot(a, m->lm_head, slot[s0]);
   a.argmax_out = argmax;
   ws_stream.window(a, lin_j++);
-  e = launch_linear_packed(L, a, st, mode * 16 + 4);
+  e = launch_linear_packed(L, a, st, mode * 16 + 4, !qkv_ready);
   return status(e);
 }
 }  // namespace
@@ -661,6 +758,13 @@ extern "C" {
 int qs_forward(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const qs_workspace_t* ws, float* logits,
                int32_t* argmax, void* stream) {
   return forward_impl(m, b, mode, ws, logits, argmax, (cudaStream_t)stream, nullptr);
+}
+
+int qs_forward_launches(void) { return g_launches; }
+
+int qs_set_emit(int32_t mask) {
+  g_emit = mask & 3;
+  return QS_OK;
 }
 
 int qs_forward_tp(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const qs_workspace_t* ws, float* logits,

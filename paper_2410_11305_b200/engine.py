@@ -106,9 +106,11 @@ class DecodeEngine:
         st = _lib.stream_ptr()
         for b, off in batches:
             _lib.call("qs_forward", self.cm, b, mode, self.ws, None, self.t["argmax"].data_ptr() + off, st)
+            self._enq += _lib.load().qs_forward_launches()
 
     # ------------------------------------------------------------------ step bodies
     def _cycle_body(self) -> None:
+        self._enq = 1 + self.gamma   # verify_prep + accept + gamma draft_preps, then forwards
         st = _lib.stream_ptr()
         for j in range(self.gamma):
             _lib.call("qs_draft_prep", self.seq, j, st)
@@ -118,19 +120,18 @@ class DecodeEngine:
         _lib.call("qs_accept", self.seq, st)
 
     def _ar_body(self) -> None:
+        self._enq = 2                # ar_prep + ar_commit, then the forward
         st = _lib.stream_ptr()
         _lib.call("qs_ar_prep", self.seq, st)
         self._forward(self.draft_batches, self.greedy_low)
         _lib.call("qs_ar_commit", self.seq, st)
 
     def launches_per_step(self) -> int:
-        """Kernels one step launches (for the bench's gpu_launches claim)."""
-        L = self.cfg.n_layers
-        # per layer: 4 packs, 4 linears, attention; + final pack + lm_head
-        fwd = 9 * L + 2
-        if self.algorithm == "qspec":
-            return self.gamma * (1 + fwd * len(self.draft_batches)) + 1 + fwd * len(self.verify_batches) + 1
-        return 2 + fwd * len(self.draft_batches)
+        """Kernels one step launches (for the bench's gpu_launches claim), counted by the
+        runtime while the step body was enqueued (qs_forward_launches)."""
+        if getattr(self, "_enq", None) is None:
+            self.step()
+        return int(self._enq)
 
     def step(self) -> None:
         """One cycle (qspec) or one token (greedy) for every slot, replayed from a CUDA graph."""

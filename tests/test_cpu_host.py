@@ -60,7 +60,10 @@ def test_workspace_sizes_7b():
                    rope_len=576)
     s = _lib.WorkspaceSizes()
     _lib.call("qs_workspace_size", m, 64, s)
-    assert s.img == 86 * 192 * 128 and s.counters == (4096 + 2) * 4
+    # two operand slots (the fused next-operand emits double-buffer the image), ascale +
+    # acorr per slot, per-tile counters + emit counters + emit leaf sums
+    assert s.img == 2 * 86 * 192 * 128 and s.ascale == 2 * 86 * 64 * 4 * 5
+    assert s.counters == (4096 + 8 + 1024 + 64 * 128) * 4
 
 
 def test_model_config_validation_mirrors_reference():
