@@ -43,6 +43,9 @@ sys.path.insert(0, ROOT)
 CFG7B = dict(n_layers=32, d_model=4096, n_heads=32, n_kv_heads=32, d_ff=11008, vocab_size=32000,
              max_seq_len=512, rope_theta=10000.0, norm_eps=1e-5, group_size=128)
 # BASELINE config 3: Llama-3-8B shape (GQA 32/8, 128k vocab), batch 32 per GPU
+# BASELINE config 4: Llama-2-13B shape, tensor parallel 2/4/8 (bench.py --tp N under torchrun)
+CFG13B = dict(n_layers=40, d_model=5120, n_heads=40, n_kv_heads=40, d_ff=13824, vocab_size=32000,
+              max_seq_len=512, rope_theta=10000.0, norm_eps=1e-5, group_size=128)
 CFG8B = dict(n_layers=32, d_model=4096, n_heads=32, n_kv_heads=8, d_ff=14336, vocab_size=128256,
              max_seq_len=512, rope_theta=500000.0, norm_eps=1e-5, group_size=128)
 METRIC = "QSpec tokens/s per GPU vs W4A16 autoregressive, 7B-shape; draft accept rate"
@@ -64,6 +67,9 @@ def parse():
     ap.add_argument("--small", action="store_true", help="tiny config (smoke / CI)")
     ap.add_argument("--model", default="7b", choices=["7b", "8b"], help="7b: Llama-2-7B shape (headline); "
                     "8b: Llama-3-8B shape (BASELINE config 3)")
+    ap.add_argument("--tp", type=int, default=0, help="BASELINE config 4: Llama-2-13B shape QSpec with tensor "
+                    "parallelism over the torchrun ranks (NCCL all-reduce + vocab-split argmax, one CUDA graph "
+                    "per cycle); the value is the group's tokens/s")
     return ap.parse_args()
 
 
@@ -372,12 +378,75 @@ def cpu_reference(a, accept_rate: float | None, n_procs: int | None = None) -> d
             "sample_wall_s": round(wall, 1)}
 
 
+# ----------------------------------------------------------------------------- TP (config 4)
+def run_tp(a, rank: int, world: int) -> None:
+    """QSpec on the 13B shape, one TP group over every rank (the same requests on all ranks)."""
+    import torch
+    import torch.distributed as td
+    import paper_2410_11305_b200 as Q
+    from paper_2410_11305_b200.tp import TPComm, TPDecodeEngine
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        td.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        td.init_process_group("gloo", rank=0, world_size=1)
+    cfg = Q.ModelConfig(**CFG13B)
+    model = Q.random_init(cfg, 0)
+    comm = TPComm.nccl(td)
+    prompts = np.random.default_rng(42).integers(0, cfg.vocab_size, size=(a.batch, a.prompt))
+    eng = TPDecodeEngine(model, comm, a.batch, gamma=a.gamma, max_new_cap=a.new + 8)
+    for b in range(a.batch):
+        eng.prefill(b, [int(t) for t in prompts[b]], a.new)
+    for _ in range(a.warmup):
+        eng.step()
+    torch.cuda.synchronize()
+    n0 = eng.t["n_out"].sum().item()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    td.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(torch.cuda.current_device())
+    clocks.start()
+    e0.record()
+    for _ in range(a.steps):
+        eng.step()
+    e1.record()
+    torch.cuda.synchronize()
+    td.barrier()
+    ck = clocks.stop()
+    ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64)
+    td.all_reduce(ms, op=td.ReduceOp.MAX) if world > 1 else None
+    ms = float(ms.item())
+    tokens = eng.t["n_out"].sum().item() - n0          # the group's tokens (identical on every rank)
+    nd, na = eng.t["n_drafted"].sum().item(), eng.t["n_accepted"].sum().item()
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC + " (config 4: 13B shape, tensor parallel)", "value": round(tokens / (ms / 1e3), 2),
+            "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+            "ms_per_step": round(ms / a.steps, 4), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "int8 (tcgen05 kind::i8), fp32 epilogue / all-reduce",
+            "data": "synthetic (LCG random-init weights, rng(42) prompts)",
+            "config": {"workload": f"llama2-13b-shape random-init W4 g128, QSpec gamma={a.gamma}, batch {a.batch}, "
+                                   f"prompt {a.prompt}, tensor parallel {world}",
+                       "parallelism": f"tp{world} (column/row split, NCCL all-reduce x2 per layer, vocab-split "
+                                      f"lm_head + all-gathered argmax)", "global_batch": a.batch},
+            "acceptance_rate": round(na / nd, 4) if nd else None,
+            "gpu_launches": int(eng.launches_per_step() * a.steps), "clocks": ck}), flush=True)
+    comm.close()
+    td.destroy_process_group()
+
+
 # ----------------------------------------------------------------------------- main
 def main() -> None:
     a = parse()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if a.tp and a.impl == "ours":
+        run_tp(a, rank, world)
+        return
     if a.impl == "reference":
         if rank != 0:
             return

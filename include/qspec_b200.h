@@ -182,6 +182,34 @@ int qs_forward(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const qs_
  * enqueued on `stream`), then added into the residual stream: one all-reduce per
  * block half, 2 per layer.  Returns the hook's failure as QS_ERR_CUDA. */
 typedef int (*qs_allreduce_fn)(float* ptr, int64_t count, void* stream, void* user);
+/* all-gather of `bytes` per rank: recv[r * bytes ..] = send of rank r (hook mode) */
+typedef int (*qs_allgather_fn)(const void* send, void* recv, int64_t bytes, void* stream, void* user);
+
+/* Tensor-parallel QSpec step (config 4; reference loop specdec.py:258-317 over a TP
+ * shard).  The model struct holds this rank's shard as for qs_forward_tp, except that
+ * lm_head is VOCAB-SPLIT: rows [vocab_off, vocab_off + m->vocab) of the full head.  The
+ * collectives run on `stream`: with nccl_comm set (qs_tp_nccl_init), ncclAllReduce of the
+ * row-split partial sums (2 per layer) and ncclAllGather of each rank's (max, index) pair
+ * per token, reduced in rank order with the lowest index winning ties (numerics.py:81-86)
+ * -- no host callback, no synchronisation, so whole draft/verify cycles capture into one
+ * CUDA graph.  With nccl_comm == NULL the two hooks are called instead (tests: gloo).
+ * `logits` (optional) receives this rank's vocab shard [T][m->vocab]; `argmax` the global
+ * token ids.  scratch: device buffer of qs_tp_scratch_bytes(world) bytes. */
+typedef struct {
+  int32_t world, rank;
+  int32_t vocab_off;
+  void* nccl_comm;
+  qs_allreduce_fn allreduce;
+  qs_allgather_fn allgather;
+  void* user;
+  void* scratch;
+} qs_tp_t;
+size_t qs_tp_scratch_bytes(int32_t world);
+int qs_tp_nccl_unique_id(uint8_t* id128);
+int qs_tp_nccl_init(int32_t world, int32_t rank, const uint8_t* id128, void** comm);
+int qs_tp_nccl_destroy(void* comm);
+int qs_forward_tp2(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const qs_workspace_t* ws, float* logits,
+                   int32_t* argmax, const qs_tp_t* tp, void* stream);
 /* kernels the last qs_forward / qs_forward_tp call enqueued (host-side count) */
 int qs_forward_launches(void);
 /* fused next-operand emits, mask: 1 = gate_up's epilogue emits down_proj's operand, 2 = the

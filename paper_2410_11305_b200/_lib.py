@@ -23,6 +23,14 @@ vp = C.c_void_p
 
 
 ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p)
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p)
+
+
+class TP(C.Structure):
+    """qs_tp_t"""
+    _fields_ = [("world", C.c_int32), ("rank", C.c_int32), ("vocab_off", C.c_int32), ("nccl_comm", C.c_void_p),
+                ("allreduce", ALLREDUCE_FN), ("allgather", ALLGATHER_FN), ("user", C.c_void_p),
+                ("scratch", C.c_void_p)]
 
 
 class QWeight(C.Structure):
@@ -87,6 +95,12 @@ _SIGS = {
     "qs_debug_timeline": ([vp], C.c_int),
     "qs_debug_select": ([i32], C.c_int),
     "qs_forward_launches": ([], C.c_int),
+    "qs_tp_scratch_bytes": ([i32], C.c_size_t),
+    "qs_tp_nccl_unique_id": ([C.POINTER(C.c_uint8)], C.c_int),
+    "qs_tp_nccl_init": ([i32, i32, C.POINTER(C.c_uint8), C.POINTER(C.c_void_p)], C.c_int),
+    "qs_tp_nccl_destroy": ([vp], C.c_int),
+    "qs_forward_tp2": ([C.POINTER(Model), C.POINTER(Batch), i32, C.POINTER(Workspace), vp, vp, C.POINTER(TP), vp],
+                       C.c_int),
     "qs_set_emit": ([i32], C.c_int),
     "qs_linear_group_dots": ([C.POINTER(QWeight), vp, i32, i32, vp, C.POINTER(Workspace), vp], C.c_int),
     "qs_profile_enable": ([i32], C.c_int),

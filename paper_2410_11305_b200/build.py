@@ -20,8 +20,20 @@ BUILD = os.environ.get("QS_BUILD_DIR") or os.path.join(HERE, "_build")
 LIB = os.environ.get("QS_LIB_OUT") or os.path.join(HERE, "libqspec_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+def _nccl_root() -> str:
+    """NCCL headers/library: the pip nvidia-nccl package torch itself loads (same soname,
+    so one libnccl.so.2 serves torch.distributed and qs_forward_tp2)."""
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia.nccl")
+    if spec and spec.submodule_search_locations:
+        return list(spec.submodule_search_locations)[0]
+    return "/usr"
+
+
+NCCL = _nccl_root()
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
-         "--expt-relaxed-constexpr", "-I", os.path.join(HERE, "..", "include")]
+         "--expt-relaxed-constexpr", "-I", os.path.join(HERE, "..", "include"), "-I", os.path.join(NCCL, "include")]
+LINK = ["-lcudart", "-L", os.path.join(NCCL, "lib"), "-l:libnccl.so.2", "-Xlinker", "-rpath=" + os.path.join(NCCL, "lib")]
 
 
 def sources() -> list[str]:
@@ -64,7 +76,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
     with cf.ThreadPoolExecutor(max_workers=min(8, max(1, len(jobs)))) as ex:
         list(ex.map(run, jobs))
     if force or jobs or _stale(LIB, objs):
-        run([NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart"])
+        run([NVCC, *ARCH, "-shared", "-o", LIB, *objs, *LINK])
     with open(stamp, "w") as f:
         f.write(flags)
     return LIB

@@ -822,7 +822,10 @@ __global__ void __launch_bounds__(512, 1) linear_tc_kernel(const LinearArgs a) {
               const int oi = ai[(size_t)tt * TMAX + et];
               if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
             }
-            a.argmax_out[et] = bi;
+            if (a.arg_rec != nullptr)
+              a.arg_rec[et] = make_int2(__float_as_int(bv), bi + a.arg_off);
+            else
+              a.argmax_out[et] = bi;
           }
           if (et == 0) a.counters[a.n_tiles] = 0;
         }

@@ -150,6 +150,8 @@ struct LinearArgs {
   float* arg_val;
   int* arg_idx;
   int* argmax_out;
+  int2* arg_rec;   // vocab-split TP: (max value bits, global index) per token instead of argmax_out
+  int arg_off;     // this shard's first vocab row
   // kOpDump
   int32_t* dump;
   // operand producer of this linear (run by a preceding act_pack launch)

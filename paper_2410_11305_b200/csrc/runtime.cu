@@ -30,6 +30,8 @@ cudaError_t launch_repack_ref(const uint8_t* ref_codes, const float* ref_scales,
                               int row_stride, cudaStream_t st);
 
 cudaError_t launch_control(int op, const SeqState& s, int j, cudaStream_t st);
+int tp_allreduce_nccl(float* p, int64_t count, void* comm, cudaStream_t st);
+int tp_argmax_reduce(const qs_tp_t* tp, int T, int32_t* argmax, cudaStream_t st);
 cudaError_t launch_add_rows(float* x, const float* y, int n, cudaStream_t st);
 }  // namespace qs
 
@@ -542,6 +544,7 @@ struct TpHooks {
   int world;
   qs_allreduce_fn fn;
   void* user;
+  const qs_tp_t* tp2;  // qs_forward_tp2: NCCL / gather hooks + vocab-split lm_head
 };
 // Operand slots: the image + scales a linear reads, and the one its epilogue emits for
 // the NEXT linear, must differ (some CTAs still stream their operand while finished
@@ -590,7 +593,8 @@ int forward_impl(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const q
   const int res_op = tp ? kOpStore : kOpResidual;
   float* res_out = tp ? ws->attn : ws->x;
   auto reduce_into_x = [&]() -> int {
-    int rc = tp->fn(ws->attn, (int64_t)T * d, st, tp->user);
+    int rc = (tp->tp2 && tp->tp2->nccl_comm) ? tp_allreduce_nccl(ws->attn, (int64_t)T * d, tp->tp2->nccl_comm, st)
+                                            : tp->fn(ws->attn, (int64_t)T * d, st, tp->user);
     if (rc != 0) return QS_ERR_CUDA;
     ++g_launches;
     return status(launch_add_rows(ws->x, ws->attn, T * d, st));
@@ -748,9 +752,15 @@ int forward_impl(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const q
   a.pk.eps = m->norm_eps;
   use_slot(a, m->lm_head, slot[s0]);
   a.argmax_out = argmax;
+  const qs_tp_t* tp2 = tp ? tp->tp2 : nullptr;
+  if (tp2) {  // vocab-split head: per-rank (max, index) records, gathered and reduced below
+    a.arg_rec = reinterpret_cast<int2*>(tp2->scratch);
+    a.arg_off = tp2->vocab_off;
+  }
   ws_stream.window(a, lin_j++);
   e = launch_linear_packed(L, a, st, mode * 16 + 4, !qkv_ready);
-  return status(e);
+  if (e != cudaSuccess || !tp2) return status(e);
+  return tp_argmax_reduce(tp2, T, argmax, st);
 }
 }  // namespace
 
@@ -762,6 +772,15 @@ int qs_forward(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const qs_
 
 int qs_forward_launches(void) { return g_launches; }
 
+int qs_forward_tp2(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const qs_workspace_t* ws, float* logits,
+                   int32_t* argmax, const qs_tp_t* tp, void* stream) {
+  if (!tp || tp->world < 1 || tp->rank < 0 || tp->rank >= tp->world || !tp->scratch) return QS_ERR_CONFIG;
+  if (!tp->nccl_comm && (!tp->allreduce || !tp->allgather)) return QS_ERR_CONFIG;
+  if (m->n_heads % m->n_kv_heads != 0 || m->d_model % (m->n_heads * tp->world) != 0) return QS_ERR_CONFIG;
+  TpHooks h{tp->world, tp->allreduce, tp->user, tp};
+  return forward_impl(m, b, mode, ws, logits, argmax, (cudaStream_t)stream, &h);
+}
+
 int qs_set_emit(int32_t mask) {
   g_emit = mask & 3;
   return QS_OK;
@@ -771,7 +790,7 @@ int qs_forward_tp(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const 
                   int32_t* argmax, int32_t world, qs_allreduce_fn allreduce, void* user, void* stream) {
   if (world < 1 || !allreduce || m->n_heads % m->n_kv_heads != 0) return QS_ERR_CONFIG;
   if (m->d_model % (m->n_heads * world) != 0) return QS_ERR_CONFIG;
-  TpHooks tp{world, allreduce, user};
+  TpHooks tp{world, allreduce, user, nullptr};
   return forward_impl(m, b, mode, ws, logits, argmax, (cudaStream_t)stream, &tp);
 }
 

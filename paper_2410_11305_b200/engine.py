@@ -51,7 +51,7 @@ class DecodeEngine:
         self.model, self.cfg, self.B, self.gamma = model, cfg, batch, gamma
         self.algorithm, self.draft_low, self.greedy_low = algorithm, draft_low, greedy_low
         self.eos = -1 if eos_token is None else int(eos_token)
-        self.kv = KVCache(cfg, gamma_max=gamma, slots=batch)
+        self._setup_storage(model, batch, gamma)
         self.cap = max_new_cap
         i32 = dict(dtype=torch.int32, device="cuda")
         B, G1 = batch, gamma + 1
@@ -70,8 +70,6 @@ class DecodeEngine:
             "n_drafted", "n_accepted", "n_cycles", "dropped", "trace", "trace_tok", "tok", "pos", "slot",
             "argmax")}, out_cap=self.cap, trace_cap=self.cap, B=B, gamma=gamma, eos=self.eos,
             max_seq=cfg.max_seq_len)
-        self.ws, self._ws_bufs = model.workspace(64)
-        self.cm = model.c_model(self.kv)
         hpk = cfg.n_heads // cfg.n_kv_heads
         if G1 * hpk > 64:
             raise ConfigError("gamma+1 query rows per kv head exceed the attention block limit (64)")
@@ -81,6 +79,20 @@ class DecodeEngine:
         self.use_graphs = use_graphs
         self.graph = None
         self.n_launch_cycle = 0
+
+    def _setup_storage(self, model: TransformerModel, batch: int, gamma: int) -> None:
+        """KV pool, workspace and the C model view the forwards run on (TP overrides)."""
+        self.kv = KVCache(model.config, gamma_max=gamma, slots=batch)
+        self.ws, self._ws_bufs = model.workspace(64)
+        self.cm = model.c_model(self.kv)
+
+    def _call_forward(self, b, mode: int, argmax_ptr: int, st: int) -> None:
+        _lib.call("qs_forward", self.cm, b, mode, self.ws, None, argmax_ptr, st)
+
+    def _prefill_argmax(self, prompt, slot: int, low: bool):
+        """argmax of every prompt position (device int32 [n]) after the HIGH prefill."""
+        _, argmax = run_forward_chunks(self.model, self.kv, prompt, 0, low, slot=slot)
+        return argmax
 
     # ------------------------------------------------------------------ batches
     def _batches(self, per_seq: int) -> list[tuple[_lib.Batch, int]]:
@@ -105,7 +117,7 @@ class DecodeEngine:
         mode = _lib.QS_MODE_LOW if low else _lib.QS_MODE_HIGH
         st = _lib.stream_ptr()
         for b, off in batches:
-            _lib.call("qs_forward", self.cm, b, mode, self.ws, None, self.t["argmax"].data_ptr() + off, st)
+            self._call_forward(b, mode, self.t["argmax"].data_ptr() + off, st)
             self._enq += _lib.load().qs_forward_launches()
 
     # ------------------------------------------------------------------ step bodies
@@ -201,7 +213,7 @@ class DecodeEngine:
                 raise TokenIdError("prompt token out of vocab range")
             prompt = [int(t) for t in prompt]
         low = self.algorithm == "greedy" and self.greedy_low
-        _, argmax = run_forward_chunks(self.model, self.kv, prompt, 0, low, slot=slot)
+        argmax = self._prefill_argmax(prompt, slot, low)
         first = argmax[len(prompt) - 1:len(prompt)]
         b = slot
         self.t["pending"][b:b + 1].copy_(first)

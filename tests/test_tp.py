@@ -90,3 +90,13 @@ def test_tp_forward_matches_single_gpu(world, tmp_path):
     ref = Q.generate_greedy(model, prompt, Q.ExecutionMode.HIGH_PRECISION,
                             Q.GenerationConfig(max_new_tokens=n_new)).new_tokens
     assert list(np.load(tmp_path / "toks.npy")) == ref
+
+
+def test_vocab_shard_tiles_cover_vocab():
+    from paper_2410_11305_b200.tp import vocab_shard
+    for V in (32000, 128256, 1024, 1000):
+        for world in (1, 2, 4, 8):
+            sh = [vocab_shard(V, r, world) for r in range(world)]
+            assert sh[0][0] == 0 and sh[-1][1] == V
+            assert all(a[1] == b[0] for a, b in zip(sh, sh[1:]))
+            assert all(v0 % 128 == 0 for v0, _ in sh)
