@@ -17,7 +17,7 @@ HEADER = os.path.join(ROOT, "include", "qspec_b200.h")
 
 def header_functions() -> list[str]:
     txt = open(HEADER).read()
-    return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(qs_\w+)\s*\(", txt, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|size_t|const char\*)\s+(qs_\w+)\s*\(", txt, re.M)))
 
 
 def test_library_exports_every_header_symbol():
