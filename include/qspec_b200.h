@@ -70,6 +70,10 @@ typedef struct {
   const qs_layer_t* layers; /* HOST array [n_layers] */
   const int32_t* block_table; /* device [slots][bt_ld] page ids */
   int32_t bt_ld, page;
+  int32_t hadamard; /* opt-in (default 0; the reference has no rotation): every linear operand
+                       group is rotated by the orthonormal 128-point Walsh-Hadamard transform
+                       before quantisation; the weights were rotated the same way when built
+                       (qs_hadamard_rows), so x.W^T is unchanged up to rounding */
 } qs_model_t;
 
 /* One forward pass: T tokens; query blocks = runs of tokens of one slot. */
@@ -133,6 +137,9 @@ int qs_repack_ref(const uint8_t* ref_codes, const float* ref_scales, int32_t row
                   uint8_t* codes, float* scales, int32_t n_pad, int32_t row_off, int32_t row_stride, void* stream);
 
 /* ------------------------------------------------------------- operators */
+/* In-place orthonormal 128-point Walsh-Hadamard transform of every 128-block of every row
+   of x [rows][cols] (cols % 128 == 0): the opt-in rotation (qs_model_t.hadamard) */
+int qs_hadamard_rows(float* x, int64_t rows, int32_t cols, void* stream);
 int qs_act_quant(const float* x, int32_t T, int32_t K, int32_t g, int8_t* codes, float* scales, float* fq,
                  void* stream);
 /* numerics.py:46-62 rmsnorm: y = (x * (1/sqrt(mean(x^2) + eps))) * w per row, bit-exact

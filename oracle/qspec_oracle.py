@@ -46,6 +46,7 @@ class OracleConfig:
     rope_theta: float = 10000.0
     norm_eps: float = 1e-5
     group_size: int = 128
+    hadamard: bool = False   # opt-in rotation of the B200 build (not in the reference; wht128)
 
     @property
     def head_dim(self) -> int:
@@ -211,6 +212,7 @@ class OracleLinear:
     scales: np.ndarray         # f32 [out, in/g]
     g: int
     _wt: np.ndarray | None = field(default=None, repr=False)
+    rotated: bool = False      # opt-in Hadamard rotation (inputs rotated by wht128 in qlinear)
 
     @property
     def wt(self) -> np.ndarray:
@@ -222,8 +224,28 @@ class OracleLinear:
         return pack_nibbles(self.codes)
 
 
+def wht128(x: np.ndarray) -> np.ndarray:
+    """The opt-in rotation (ModelConfig.hadamard; NOT part of the reference, which has no
+    rotation -- SPEC.md:17): orthonormal 128-point Walsh-Hadamard transform of every
+    128-block along the last axis, float32 butterflies over index bits 0..6 in order
+    (pair (i, i | 2^b) -> a + c, a - c), then * f32(1/sqrt(128)) -- csrc/pack_dev.cuh
+    wht128_warp's order, so rotated codes compare bit for bit."""
+    x = np.asarray(x, dtype=np.float32)
+    shp = x.shape
+    y = x.reshape(-1, 128).copy()
+    h = 1
+    while h < 128:
+        y = y.reshape(-1, 128 // (2 * h), 2, h)
+        a, c = y[:, :, 0, :], y[:, :, 1, :]
+        y = np.stack([a + c, a - c], axis=2).reshape(-1, 128)
+        h *= 2
+    return (y * np.float32(1.0 / np.sqrt(128.0))).reshape(shp)
+
+
 def qlinear(lin: OracleLinear, x: np.ndarray, low: bool) -> np.ndarray:
     """quant.py:248-261 with numerics.py:31-43 (einsum, optimize=False)."""
+    if lin.rotated:
+        x = wht128(x)
     if low:
         x = fake_quant(x, lin.g)
     return np.einsum("ik,kj->ij", x, lin.wt, optimize=False)
@@ -315,8 +337,9 @@ class OracleModel:
 
 def build_model(cfg: OracleConfig, tensors: dict[str, np.ndarray]) -> OracleModel:
     def q(name: str) -> OracleLinear:
-        codes, s = quantize_rows(tensors[name], cfg.group_size)
-        return OracleLinear(codes, s, cfg.group_size)
+        w = wht128(tensors[name]) if cfg.hadamard else tensors[name]
+        codes, s = quantize_rows(w, cfg.group_size)
+        return OracleLinear(codes, s, cfg.group_size, rotated=cfg.hadamard)
 
     layers = []
     for i in range(cfg.n_layers):

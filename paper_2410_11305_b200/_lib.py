@@ -48,7 +48,7 @@ class Model(C.Structure):
                                    "group_size", "rope_len")] + [
         ("norm_eps", f32), ("tok_emb", vp), ("final_norm", vp), ("rope_cos", vp), ("rope_sin", vp),
         ("lm_head", QWeight), ("layers", C.POINTER(Layer)), ("block_table", vp), ("bt_ld", i32),
-        ("page", i32)]
+        ("page", i32), ("hadamard", i32)]
 
 
 class Batch(C.Structure):
@@ -95,6 +95,7 @@ _SIGS = {
     "qs_debug_timeline": ([vp], C.c_int),
     "qs_debug_select": ([i32], C.c_int),
     "qs_forward_launches": ([], C.c_int),
+    "qs_hadamard_rows": ([vp, i64, i32, vp], C.c_int),
     "qs_tp_scratch_bytes": ([i32], C.c_size_t),
     "qs_tp_nccl_unique_id": ([C.POINTER(C.c_uint8)], C.c_int),
     "qs_tp_nccl_init": ([i32, i32, C.POINTER(C.c_uint8), C.POINTER(C.c_void_p)], C.c_int),

@@ -50,4 +50,23 @@ cudaError_t launch_act_pack(int L, const PackArgs& a, cudaStream_t st) {
   return launch_k(act_pack_kernel<3, false, false>, grid, dim3(kPackThreads), 0, st, a);
 }
 
+// qs_hadamard_rows: one warp per (row, 128-block), in place (the weight rotation of the
+// opt-in ModelConfig.hadamard, and the standalone API's activation rotation)
+__global__ void __launch_bounds__(256) hadamard_rows_kernel(float* __restrict__ x, long long blocks) {
+  const long long b = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (b >= blocks) return;
+  float4* p = reinterpret_cast<float4*>(x + b * 128) + lane;
+  const float4 in = *p;
+  float v[4] = {in.x, in.y, in.z, in.w};
+  wht128_warp(v, lane);
+  *p = make_float4(v[0], v[1], v[2], v[3]);
+}
+
+cudaError_t launch_hadamard_rows(float* x, long long rows, int cols, cudaStream_t st) {
+  const long long blocks = rows * (cols / 128);
+  hadamard_rows_kernel<<<(unsigned)((blocks + 7) / 8), 256, 0, st>>>(x, blocks);
+  return cudaGetLastError();
+}
+
 }  // namespace qs

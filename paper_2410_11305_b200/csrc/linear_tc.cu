@@ -261,7 +261,7 @@ __device__ __forceinline__ void emit_rms(const LinearArgs& a, float* stg, int ti
     const float4 wv = *reinterpret_cast<const float4*>(a.e_rms_w + (size_t)tile * 128 + 4 * lane);
     const float v[4] = {__fmul_rn(__fmul_rn(xv.x, iv), wv.x), __fmul_rn(__fmul_rn(xv.y, iv), wv.y),
                         __fmul_rn(__fmul_rn(xv.z, iv), wv.z), __fmul_rn(__fmul_rn(xv.w, iv), wv.w)};
-    quant_group_warp<L>(v, t, tile, lane, a.e_img, a.e_ascale, a.e_acorr, a.r_pad, a.a_ld);
+    quant_group_warp<L>(v, t, tile, lane, a.e_img, a.e_ascale, a.e_acorr, a.r_pad, a.a_ld, a.e_rotate != 0);
   }
 }
 
@@ -280,7 +280,7 @@ __device__ __forceinline__ void emit_silu(const LinearArgs& a, int tile, int et,
   for (int t = ew; t < a.T; t += kEpiWarps) {
     const float4 hv = __ldcg(reinterpret_cast<const float4*>(a.out + (size_t)t * a.ldo + 128 * q) + lane);
     const float v[4] = {hv.x, hv.y, hv.z, hv.w};
-    quant_group_warp<L>(v, t, q, lane, a.e_img, a.e_ascale, a.e_acorr, a.r_pad, a.a_ld);
+    quant_group_warp<L>(v, t, q, lane, a.e_img, a.e_ascale, a.e_acorr, a.r_pad, a.a_ld, a.e_rotate != 0);
   }
   if (et == 0) a.e_cnt[8 + q] = 0;
 }

@@ -182,14 +182,43 @@ __device__ __forceinline__ float token_inv_rms(const PackArgs& a, int t, int tid
   return __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(ms, a.eps)));
 }
 
+// Opt-in block rotation (ModelConfig.hadamard, default off; the reference has none --
+// SPEC.md:17): the orthonormal 128-point Walsh-Hadamard transform of one group, lane
+// holding elements 4*lane..+3.  Butterfly stages over index bits 0..6 in order (pair
+// (i, i | 2^b): a + c, a - c), then * f32(1/sqrt(128)) -- the order oracle/
+// qspec_oracle.py wht128 restates, so rotated codes are bit-exact too.
+constexpr float kInvSqrt128 = 0.08838834764831845f;
+__device__ __forceinline__ void wht128_warp(float (&v)[4], int lane) {
+  float t0 = __fadd_rn(v[0], v[1]), t1 = __fsub_rn(v[0], v[1]);
+  float t2 = __fadd_rn(v[2], v[3]), t3 = __fsub_rn(v[2], v[3]);
+  v[0] = __fadd_rn(t0, t2);
+  v[2] = __fsub_rn(t0, t2);
+  v[1] = __fadd_rn(t1, t3);
+  v[3] = __fsub_rn(t1, t3);
+#pragma unroll
+  for (int m = 1; m < 32; m <<= 1) {
+    const bool hi = (lane & m) != 0;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float o = __shfl_xor_sync(0xffffffffu, v[e], m);
+      v[e] = hi ? __fsub_rn(o, v[e]) : __fadd_rn(v[e], o);
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < 4; ++e) v[e] = __fmul_rn(v[e], kInvSqrt128);
+}
+
 // One warp quantises one 128-element group of token t (lane holds elements 4*lane..+3,
 // already normalised) into chunk `ch` of the operand image + its activation scale and
 // offset-binary correction sums -- the same arithmetic as pack_group's plain path (the
 // linear epilogues use it to emit the NEXT linear's operand; tests check the fused and
 // the act_pack operands are bit-identical).
 template <int L>
-__device__ __forceinline__ void quant_group_warp(const float (&v)[4], int t, int ch, int lane, uint8_t* img,
-                                                 float* ascale, int32_t* acorr, int r_pad, int a_ld) {
+__device__ __forceinline__ void quant_group_warp(const float (&vin)[4], int t, int ch, int lane, uint8_t* img,
+                                                 float* ascale, int32_t* acorr, int r_pad, int a_ld,
+                                                 bool rotate = false) {
+  float v[4] = {vin[0], vin[1], vin[2], vin[3]};
+  if (rotate) wht128_warp(v, lane);
   float m = fmaxf(fmaxf(fabsf(v[0]), fabsf(v[1])), fmaxf(fabsf(v[2]), fabsf(v[3])));
   m = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(m)));
   float s, mul;
@@ -290,6 +319,10 @@ __device__ __forceinline__ void pack_group(const PackArgs& a, int t, int gi, flo
       val[it][e] = v;
       m = fmaxf(m, fabsf(v));
     }
+  }
+  if (kLean && a.rotate) {  // opt-in Hadamard rotation of the group (g == gp == 128)
+    wht128_warp(val[0], lane);
+    m = fmaxf(fmaxf(fabsf(val[0][0]), fabsf(val[0][1])), fmaxf(fabsf(val[0][2]), fabsf(val[0][3])));
   }
   // group max|x| in one warp reduction: non-negative floats order like their bit patterns
   m = __uint_as_float(__reduce_max_sync(0xffffffffu, __float_as_uint(m)));

@@ -108,6 +108,7 @@ struct PackArgs {
   uint8_t* img;
   float* ascale;
   int32_t* acorr;  // [n_chunks][a_ld][4] offset-binary correction sums (with img)
+  int rotate;      // opt-in 128-point Hadamard rotation of every group before quantising
   int8_t* codes_out;
   float* scales_out;
   float* fq_out;
@@ -182,6 +183,7 @@ struct LinearArgs {
   int e_n;         // row width (the RMSNorm mean's n)
   float* e_leaf;   // [T][n_tiles]
   int* e_cnt;      // [0] arrive, [1] depart (kEmitRms); [8 + q] per group (kEmitSilu); zero on entry and exit
+  int e_rotate;    // Hadamard-rotate the emitted groups (model option)
   // debug timeline (CTA 0): [role][i] globaltimer ns; roles: 0 producer issue, 1 unpack done,
   // 2 mma issued, 3 epilogue start (acc ready), 4 epilogue done
   unsigned long long* dbg;

@@ -33,6 +33,7 @@ cudaError_t launch_control(int op, const SeqState& s, int j, cudaStream_t st);
 int tp_allreduce_nccl(float* p, int64_t count, void* comm, cudaStream_t st);
 int tp_argmax_reduce(const qs_tp_t* tp, int T, int32_t* argmax, cudaStream_t st);
 cudaError_t launch_add_rows(float* x, const float* y, int n, cudaStream_t st);
+cudaError_t launch_hadamard_rows(float* x, long long rows, int cols, cudaStream_t st);
 }  // namespace qs
 
 using namespace qs;
@@ -120,7 +121,8 @@ namespace {
 
 // Launch a linear whose operand comes from a.pk: a separate act_pack launch
 // overlapped via PDL, then the linear.
-int g_launches = 0;  // kernels enqueued by the last qs_forward (qs_forward_launches)
+thread_local int g_launches = 0;  // kernels enqueued by the last qs_forward (qs_forward_launches)
+thread_local int g_rotate = 0;    // qs_model_t.hadamard of the forward being enqueued (pack_args / set_emit)
 
 cudaError_t launch_linear_packed(int L, LinearArgs& a, cudaStream_t st, int32_t tag = -1, bool pack = true) {
   const int32_t mode_bits = 16 * (L == 1 ? 1 : 0);
@@ -164,6 +166,7 @@ void fill_geometry(int n, int k, int g, qs_qweight_t* w) {
 
 PackArgs pack_args(const qs_qweight_t& w, const float* x, int ldx, int T, const qs_workspace_t* ws, int L) {
   PackArgs p{};
+  p.rotate = g_rotate;
   p.x = x;
   p.ldx = ldx;
   p.T = T;
@@ -463,6 +466,12 @@ int qs_repack_ref(const uint8_t* ref_codes, const float* ref_scales, int32_t row
                                   geo.G, row_off, row_stride, (cudaStream_t)stream));
 }
 
+int qs_hadamard_rows(float* x, int64_t rows, int32_t cols, void* stream) {
+  if (!x || rows < 0 || cols % 128 != 0) return QS_ERR_SHAPE;
+  if (rows == 0) return QS_OK;
+  return status(launch_hadamard_rows(x, rows, cols, (cudaStream_t)stream));
+}
+
 int qs_act_quant(const float* x, int32_t T, int32_t K, int32_t g, int8_t* codes, float* scales, float* fq,
                  void* stream) {
   if (g < 1 || K % g != 0) return QS_ERR_CONFIG;
@@ -571,6 +580,7 @@ void set_emit(LinearArgs& a, int kind, const qs_qweight_t& next, const Slot& sl,
   a.e_eps = eps;
   a.e_n = n;
   a.e_cnt = ws->counters + kGbarOffset;
+  a.e_rotate = g_rotate;
   a.e_leaf = reinterpret_cast<float*>(ws->counters + kGbarOffset + kEmitCnt);
 }
 int g_emit = -1;  // fused next-operand emits (mask: 1 silu, 2 rmsnorm): -1 = QS_EMIT env (default 3)
@@ -587,6 +597,11 @@ int forward_impl(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const q
   const int world = tp ? tp->world : 1;
   const int d = m->d_model, H = m->n_heads, KV = m->n_kv_heads, hd = d / (H * world), ff = m->d_ff;
   g_launches = 0;
+  g_rotate = m->hadamard ? 1 : 0;
+  struct RotReset {
+    ~RotReset() { g_rotate = 0; }
+  } rot_reset;  // the standalone linear API never rotates
+  if (m->hadamard && m->group_size != 128) return QS_ERR_CONFIG;
   // tensor parallel: o_proj / down_proj are row-split, so their outputs are partial
   // sums -> store into ws->attn, all-reduce (caller's hook, e.g. NCCL on this
   // stream), then add into the residual stream

@@ -50,6 +50,11 @@ class ModelConfig:
     rope_theta: float = 10000.0
     norm_eps: float = 1e-5
     group_size: int = DEFAULT_GROUP_SIZE
+    # Opt-in, default off (the reference has no rotation): rotate
+    # every linear's input groups and weight rows by the orthonormal 128-point Hadamard
+    # transform before quantising (x H . (W H)^T = x W^T; spreads activation outliers for the
+    # W4A4 draft).  Off, every result is the reference's; on, it needs group_size 128.
+    hadamard: bool = False
 
     def __post_init__(self) -> None:
         for name in ("n_layers", "d_model", "n_heads", "n_kv_heads", "d_ff", "vocab_size", "max_seq_len",
@@ -66,6 +71,8 @@ class ModelConfig:
             raise ConfigError("head dimension must be even for rotary embeddings")
         if self.rope_theta <= 0 or self.norm_eps <= 0:
             raise ConfigError("rope_theta and norm_eps must be positive")
+        if self.hadamard and self.group_size != 128:
+            raise ConfigError("the Hadamard rotation works on 128-wide groups (group_size must be 128)")
 
     @property
     def head_dim(self) -> int:
@@ -112,6 +119,8 @@ def make_layer_stores(cfg: ModelConfig, attn_norm, ffn_norm) -> LayerWeights:
     lw.gate_proj = QuantizedTensor(ff, d, g, gu, 0, 2)
     lw.up_proj = QuantizedTensor(ff, d, g, gu, 1, 2)
     lw.down_proj = QuantizedTensor(d, ff, g, dn)
+    for p in PROJ_NAMES:
+        getattr(lw, p).rotated = cfg.hadamard
     return lw
 
 
@@ -168,7 +177,7 @@ class TransformerModel:
                        tok_emb=self.token_embedding.data_ptr(), final_norm=self.final_norm.data_ptr(),
                        rope_cos=self.rope_cos.data_ptr(), rope_sin=self.rope_sin.data_ptr(),
                        lm_head=self.lm_head.store.geo, block_table=kv.block_table.data_ptr(),
-                       bt_ld=kv.block_table.shape[1], page=kv.page)
+                       bt_ld=kv.block_table.shape[1], page=kv.page, hadamard=int(cfg.hadamard))
         layers = (_lib.Layer * cfg.n_layers)()
         for i in range(cfg.n_layers):
             layers[i] = self._c_layers[i]

@@ -144,6 +144,7 @@ class QuantizedTensor:
     store: DeviceStore = field(repr=False)
     row_off: int = 0
     row_stride: int = 1
+    rotated: bool = False   # weights Hadamard-rotated (ModelConfig.hadamard): inputs are rotated too
 
     def __post_init__(self) -> None:
         if self.in_features % self.group_size:
@@ -177,8 +178,21 @@ class QuantizedTensor:
 
 
 # ---------------------------------------------------------------- construction
-def quantize_groupwise(w, group_size: int = DEFAULT_GROUP_SIZE) -> QuantizedTensor:
-    """quant.py:197-218 on the device: float32 [out, in] -> one standalone store."""
+def hadamard_rows(x):
+    """Orthonormal 128-point Walsh-Hadamard transform of every 128-block of every row (a new
+    device float32 tensor): the opt-in rotation (ModelConfig.hadamard)."""
+    import torch
+    t = torch.as_tensor(x, dtype=torch.float32).to("cuda").clone().contiguous()
+    if t.dim() != 2 or t.shape[1] % 128:
+        raise ShapeError("hadamard_rows needs a [rows, 128*k] matrix")
+    _lib.call("qs_hadamard_rows", t.data_ptr(), t.shape[0], t.shape[1], _lib.stream_ptr())
+    return t
+
+
+def quantize_groupwise(w, group_size: int = DEFAULT_GROUP_SIZE, *, hadamard: bool = False) -> QuantizedTensor:
+    """quant.py:197-218 on the device: float32 [out, in] -> one standalone store.
+    hadamard=True (opt-in, not in the reference): rotate the rows' 128-blocks first; the
+    store then rotates its inputs in qlinear_forward."""
     import torch
     _lib.require_cuda()
     t = torch.as_tensor(w)
@@ -187,11 +201,15 @@ def quantize_groupwise(w, group_size: int = DEFAULT_GROUP_SIZE) -> QuantizedTens
     if group_size < 1 or t.shape[1] % group_size:
         raise ConfigError(f"cols {t.shape[1]} not divisible by group_size {group_size}")
     t = t.to("cuda").contiguous()
+    if hadamard:
+        if group_size != 128:
+            raise ConfigError("the Hadamard rotation works on 128-wide groups")
+        t = hadamard_rows(t)
     n, k = t.shape
     st = DeviceStore.empty(n, k, group_size)
     _lib.call("qs_quantize_weight", t.data_ptr(), n, k, group_size, st.codes.data_ptr(),
               st.scales.data_ptr(), st.geo.n_pad, 0, 1, None, None, _lib.stream_ptr())
-    return QuantizedTensor(n, k, group_size, st)
+    return QuantizedTensor(n, k, group_size, st, rotated=hadamard)
 
 
 def dequantize(q: QuantizedTensor) -> np.ndarray:
@@ -282,6 +300,8 @@ def qlinear_forward(q: QuantizedTensor, x, mode: ExecutionMode):
     if t.shape[1] != q.in_features:
         raise ShapeError(f"qlinear input width {t.shape[1]} != in_features {q.in_features}")
     _log_qlinear(q, mode)
+    if q.rotated:
+        t = hadamard_rows(t)
     st = q.store
     low = mode is ExecutionMode.LOW_PRECISION
     if low:

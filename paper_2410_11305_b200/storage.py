@@ -71,6 +71,23 @@ def random_init(cfg: ModelConfig, seed: int) -> TransformerModel:
     st = _lib.stream_ptr()
     _lib.call("qs_lcg_fill", emb.data_ptr(), seed, offs["token_embedding"], emb.numel(), scale, st)
     g = cfg.group_size
+    if cfg.hadamard:  # opt-in rotation: float draws -> rotated rows -> quantise (not in the reference)
+        def init(q_rows, q_cols, off, store, row_off, stride):
+            w = torch.empty(q_rows * q_cols, dtype=torch.float32, device="cuda")
+            _lib.call("qs_lcg_fill", w.data_ptr(), seed, off, w.numel(), scale, st)
+            _lib.call("qs_hadamard_rows", w.data_ptr(), q_rows, q_cols, st)
+            _lib.call("qs_quantize_weight", w.data_ptr(), q_rows, q_cols, g, store.codes.data_ptr(),
+                      store.scales.data_ptr(), store.geo.n_pad, row_off, stride, None, None, st)
+            torch.cuda.current_stream().synchronize()
+        for i, lw in enumerate(layers):
+            for proj in ("q_proj", "k_proj", "v_proj", "o_proj", "gate_proj", "up_proj", "down_proj"):
+                q = getattr(lw, proj)
+                store, off, stride = _placement(cfg, lw, proj)
+                init(q.out_features, q.in_features, offs[f"layers.{i}.{proj}"], store, off, stride)
+        init(cfg.vocab_size, cfg.d_model, offs["lm_head"], lm, 0, 1)
+        final = torch.ones(cfg.d_model, dtype=torch.float32, device="cuda")
+        return TransformerModel(cfg, emb, layers, final,
+                                QuantizedTensor(cfg.vocab_size, cfg.d_model, g, lm, rotated=True))
     for i, lw in enumerate(layers):
         for proj in ("q_proj", "k_proj", "v_proj", "o_proj", "gate_proj", "up_proj", "down_proj"):
             q: QuantizedTensor = getattr(lw, proj)
@@ -97,23 +114,30 @@ def model_from_float_tensors(cfg: ModelConfig, tensors: dict) -> TransformerMode
     emb.copy_(dev(tensors["token_embedding"]))
     g, st = cfg.group_size, _lib.stream_ptr()
     keep = []
+    rot = (lambda w: _rotate(w)) if cfg.hadamard else (lambda w: w)
     for i, lw in enumerate(layers):
         lw.attn_norm.copy_(dev(tensors[f"layers.{i}.attn_norm"]))
         lw.ffn_norm.copy_(dev(tensors[f"layers.{i}.ffn_norm"]))
         for proj in ("q_proj", "k_proj", "v_proj", "o_proj", "gate_proj", "up_proj", "down_proj"):
             q = getattr(lw, proj)
             store, off, stride = _placement(cfg, lw, proj)
-            w = dev(tensors[f"layers.{i}.{proj}"])
+            w = rot(dev(tensors[f"layers.{i}.{proj}"]))
             keep.append(w)
             _lib.call("qs_quantize_weight", w.data_ptr(), q.out_features, q.in_features, g, store.codes.data_ptr(),
                       store.scales.data_ptr(), store.geo.n_pad, off, stride, None, None, st)
-    w = dev(tensors["lm_head"])
+    w = rot(dev(tensors["lm_head"]))
     keep.append(w)
     _lib.call("qs_quantize_weight", w.data_ptr(), cfg.vocab_size, cfg.d_model, g, lm.codes.data_ptr(),
               lm.scales.data_ptr(), lm.geo.n_pad, 0, 1, None, None, st)
     torch.cuda.synchronize()
     final = dev(tensors["final_norm"])
-    return TransformerModel(cfg, emb, layers, final, QuantizedTensor(cfg.vocab_size, cfg.d_model, g, lm))
+    return TransformerModel(cfg, emb, layers, final,
+                            QuantizedTensor(cfg.vocab_size, cfg.d_model, g, lm, rotated=cfg.hadamard))
+
+
+def _rotate(w):
+    from .quant import hadamard_rows
+    return hadamard_rows(w)
 
 
 # ---------------------------------------------------------------------------
@@ -131,8 +155,11 @@ _PROJS = ("q_proj", "k_proj", "v_proj", "o_proj", "gate_proj", "up_proj", "down_
 
 def config_to_text(cfg: ModelConfig) -> str:
     """storage.py:189-194: key=value lines, fixed order, floats by repr."""
-    return "".join(f"{f}={getattr(cfg, f)!r}\n" if f in _FLOATS else f"{f}={getattr(cfg, f)}\n"
-                   for f in HEADER_FIELDS)
+    txt = "".join(f"{f}={getattr(cfg, f)!r}\n" if f in _FLOATS else f"{f}={getattr(cfg, f)}\n"
+                  for f in HEADER_FIELDS)
+    # the opt-in rotation (not a reference field) is written only when on, so default
+    # checkpoints stay byte-identical with the reference's
+    return txt + ("hadamard=1\n" if getattr(cfg, "hadamard", False) else "")
 
 
 def config_from_text(text: str) -> ModelConfig:
@@ -150,6 +177,7 @@ def config_from_text(text: str) -> ModelConfig:
     missing = [f for f in HEADER_FIELDS if f not in vals]
     if missing:
         raise CheckpointError(f"header missing fields: {', '.join(missing)}")
+    hadamard = vals.pop("hadamard", "0") not in ("0", "False", "false")
     extra = [k for k in vals if k not in HEADER_FIELDS]
     if extra:
         raise CheckpointError(f"header has unknown fields: {', '.join(extra)}")
@@ -158,7 +186,7 @@ def config_from_text(text: str) -> ModelConfig:
     except ValueError as exc:
         raise CheckpointError(f"header value: {exc}") from exc
     try:
-        return ModelConfig(**kw)
+        return ModelConfig(**kw, hadamard=hadamard)
     except ConfigError as exc:
         raise CheckpointError(f"header config invalid: {exc}") from exc
 

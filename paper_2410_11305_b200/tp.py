@@ -151,7 +151,7 @@ class TPShard:
                              final_norm=model.final_norm.data_ptr(), rope_cos=model.rope_cos.data_ptr(),
                              rope_sin=model.rope_sin.data_ptr(), lm_head=self.lm_head.geo,
                              layers=self._c_layers, block_table=self.block_table.data_ptr(),
-                             bt_ld=self.block_table.shape[1], page=self.page)
+                             bt_ld=self.block_table.shape[1], page=self.page, hadamard=int(cfg.hadamard))
         # workspace sized for the full model (a superset of the shard's needs)
         self.ws, self._bufs = model.workspace(64)
         import torch as _t
