@@ -248,10 +248,8 @@ def linear_roofline(model, a, prof: list, batch: int, ctx_mean: float) -> dict:
     (events on the stream the kernels run on; qs_profile_* brackets every launch of one
     replayed step, tag = mode*16 + kind, mode 1 = W4A4 draft, 0 = W4A16 verify).
 
-    Per-step path (default): the dominant kernel is linear_tc_kernel; bytes per launch =
-    N*K/2 codes + 4*N*K/g scales + 4*T*K activations + 4*T*N outputs.
-    Persistent path (QSPEC_PERSISTENT=1): one forward_mk_kernel launch per forward; bytes =
-    the same linear terms for every linear of the forward + fp32 K,V of every context row.
+    The dominant kernel is linear_tc_kernel; bytes per launch = N*K/2 codes + 4*N*K/g
+    scales + 4*T*K activations + 4*T*N outputs.
     """
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     peak = peaks["hbm_gbs"]
@@ -260,16 +258,13 @@ def linear_roofline(model, a, prof: list, batch: int, ctx_mean: float) -> dict:
     names = ["qkv", "o", "gate_up", "down", "lm_head", "pack", "attention", "forward"]
     kinds, other = {}, {}
     tot_b = tot_ms = step_ms = 0.0
-    persistent = any(tag % 16 == 7 for _, tag in prof)
     for ms, tag in prof:
         mode, kind = tag // 16, tag % 16
         step_ms += ms
         draft = mode == 1
         T = batch if draft else batch * (a.gamma + 1)
         key = ("draft" if draft else "verify") + "." + names[kind]
-        if kind == 7:
-            byts = forward_bytes(model, T, batch * (ctx_mean + (1 if draft else a.gamma + 1)))
-        elif kind < 5 and not persistent:
+        if kind < 5:
             st = stores[kind]
             outw = st.n // 2 if kind == 2 else st.n
             byts = st.n * st.k / 2 + 4 * st.n * st.k / st.g + 4 * T * st.k + 4 * T * outw
@@ -289,12 +284,11 @@ def linear_roofline(model, a, prof: list, batch: int, ctx_mean: float) -> dict:
                "GBps": round(v[2] / (v[1] / 1e3) / 1e9, 1)} for k, v in kinds.items()}
     per.update({k: {"launches": v[0], "avg_us": round(1e3 * v[1] / v[0], 2)} for k, v in other.items()})
     n = sum(v[0] for v in kinds.values())
-    kernel = ("forward_mk_kernel (persistent forward)" if persistent
-              else "linear_tc_kernel (tcgen05 kind::i8), all launches of one replayed step")
+    kernel = "linear_tc_kernel (tcgen05 kind::i8), all launches of one replayed step"
     # DRAM traffic of one captured launch of the dominant kernel (committed ncu summary)
     traffic, traffic_note = None, None
     tf = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tf) and not persistent:
+    if os.path.exists(tf):
         t = json.load(open(tf))
         traffic = t["dram_bytes_per_launch"]
         k = per.get(t["per_kind"])

@@ -59,3 +59,9 @@ for i in range(64):
     if d[i] == 0:
         break
     print(f"{i:3d} " + " ".join(f"{(d[r * 64 + i] - t0) if d[r * 64 + i] else -1:8d}" for r in (4, 5, 6, 7, 8, 9, 10)))
+
+print(" i  epi_top  sfull_ok  acc_ok(epi_start)  ld_done  epi_done")
+for i in range(64):
+    if d[i] == 0:
+        break
+    print(f"{i:3d} " + " ".join(f"{(d[r * 64 + i] - t0) if d[r * 64 + i] else -1:8d}" for r in (11, 12, 10, 13, 3)))
