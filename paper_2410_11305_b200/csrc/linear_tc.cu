@@ -46,6 +46,9 @@
 #ifndef QS_ONE_ACC
 #define QS_ONE_ACC 0
 #endif
+#ifndef QS_EPI16_TMIN
+#define QS_EPI16_TMIN 32
+#endif
 // research ablations (scripts/lin_ablate.sh), 0 in the product build; bit 0: unpack skips
 // LDS + ALU, 1: no MMAs (commits only), 2: epilogue skips TMEM loads + math, 3: unpack
 // skips tcgen05.st, 4: no weight bulk copies (the ring fills without HBM traffic)
@@ -86,7 +89,11 @@ struct LinCfg {
   // quadrant each).  Small T is unpack-bound -> 8 unpack warps; large T is
   // epilogue-bound -> 8 epilogue warps.
   static constexpr int kUnpackWarps = TMAX <= QS_UNPACK8_TMAX ? 8 : 4;
-  static constexpr int kEpiWarps = 12 - kUnpackWarps;
+  // T >= 32 buckets are epilogue-latency bound (one 3-limb chunk drain + scale-accumulate
+  // per stage, only two accumulator buffers fit TMEM): 16 epilogue warps (4 per TMEM lane
+  // quadrant, 2 token chunks each) in a 768-thread CTA halve each warp's per-chunk chain
+  static constexpr int kEpiWarps = TMAX >= QS_EPI16_TMIN ? 16 : 12 - kUnpackWarps;
+  static constexpr int kThreads = 32 * (4 + kUnpackWarps + kEpiWarps);
   static constexpr int kEpiHalves = kEpiWarps / 4;
   static constexpr int kUnpackHalves = kUnpackWarps / 4;
   // residual-emit staging: the tile's new residual rows [T][128] + 1/rms per token
@@ -286,7 +293,7 @@ __device__ __forceinline__ void emit_silu(const LinearArgs& a, int tile, int et,
 }
 
 template <int L, int TMAX, int OPC>
-__global__ void __launch_bounds__(512, 1) linear_tc_kernel(const LinearArgs a) {
+__global__ void __launch_bounds__(LinCfg<L, TMAX>::kThreads, 1) linear_tc_kernel(const LinearArgs a) {
   using C = LinCfg<L, TMAX>;
   constexpr int CPS = C::kCPS;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -495,7 +502,7 @@ __global__ void __launch_bounds__(512, 1) linear_tc_kernel(const LinearArgs a) {
       tc_fence_after();
       if (dbg0 && i < 64 && r == 0) a.dbg[9 * 64 + i] = gtimer();
       // all LDS of the stage first (latency overlap), then unpack + TMEM stores
-      constexpr int kPre = CPS <= 4 ? CPS : 1;  // register budget
+      constexpr int kPre = C::kThreads > 512 ? 1 : (CPS <= 4 ? CPS : 1);  // register budget
       uint4 wv[CPS][4];
 #pragma unroll
       for (int q = 0; q < kPre; ++q) {
@@ -593,7 +600,7 @@ __global__ void __launch_bounds__(512, 1) linear_tc_kernel(const LinearArgs a) {
         constexpr int kCols = C::kTokChunk * L;
         constexpr int KC = kCols <= 8 ? 8 : (kCols <= 16 ? 16 : 24);
         // double-buffer only where the registers allow (no spills under the 128 cap)
-        constexpr bool kPipe = 2 * CPS * KC <= 64;
+        constexpr bool kPipe = C::kThreads <= 512 && 2 * CPS * KC <= 64;
         uint32_t rb[kPipe ? 2 : 1][CPS][KC];
         auto issue = [&](int lc, uint32_t (&rr)[CPS][KC]) {
 #pragma unroll
@@ -707,7 +714,7 @@ __global__ void __launch_bounds__(512, 1) linear_tc_kernel(const LinearArgs a) {
           if (QS_LIN_TIMELINE && a.dbg) a.dbg[5120 + c] = gtimer();
         }
         named_bar(1, kEpiT);
-        constexpr int kPB = kOwn <= 1 ? 4 : (kOwn == 2 ? 2 : 1);
+        constexpr int kPB = C::kThreads > 512 ? 1 : (kOwn <= 1 ? 4 : (kOwn == 2 ? 2 : 1));
         for (int cb = c_lo + 1; cb <= c_hi; cb += kPB) {
           float pv[kPB][kOwn * 8];
 #pragma unroll
@@ -863,7 +870,7 @@ static cudaError_t launch_linear_op(const LinearArgs& a, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     if (dev < kMaxDevices) attr[dev] = true;
   }
-  return launch_k(linear_tc_kernel<L, TMAX, OPC>, dim3(a.n_cta), dim3(512), C::kSmemBytes, st, a);
+  return launch_k(linear_tc_kernel<L, TMAX, OPC>, dim3(a.n_cta), dim3(C::kThreads), C::kSmemBytes, st, a);
 }
 
 template <int L, int TMAX>
