@@ -179,6 +179,7 @@ def run_decode(model, a, batch: int, algorithm: str, prompts: np.ndarray, steps:
     if profile:
         out["ctx_mean"] = float(eng.t["committed"].float().mean().item())
         out["profile"] = eng.profile_step()
+        out["ktrace"] = eng.ktrace_step()
     del eng
     torch.cuda.empty_cache()
     return out
@@ -241,6 +242,30 @@ def forward_bytes(model, T: int, ctx_sum: float) -> float:
     tot += h.n * h.k / 2 + 4 * h.n * h.k / h.g + 4 * T * h.k + 4 * T * h.n
     tot += ctx_sum * cfg.n_layers * cfg.n_kv_heads * cfg.head_dim * 2 * 4
     return tot
+
+
+def critical_path(kt) -> dict:
+    """Exposed (critical-path) time per kernel kind in the real replayed graph (PDL intact):
+    launch i adds end_i - max(start_i, latest end of the launches before it).  The event-
+    bracketed per-launch durations above serialise the graph; this is where the step's time
+    actually goes."""
+    tags, st, en = kt
+    names = ["qkv", "o", "gate_up", "down", "lm_head", "pack", "attention"]
+    per, prev, span = {}, 0.0, float(en.max()) if len(en) else 0.0
+    for i in range(len(tags)):
+        mode, kind = tags[i] // 16, tags[i] % 16
+        key = ("draft." if mode == 1 else "verify.") + (names[kind] if kind < len(names) else "linear")
+        exp = max(0.0, en[i] - max(st[i], prev))
+        prev = max(prev, en[i])
+        d = per.setdefault(key, [0, 0.0])
+        d[0] += 1
+        d[1] += exp
+    lin = sum(v[1] for k, v in per.items() if k.split(".")[1] in names[:5])
+    return {"span_us": round(span, 1), "linear_exposed_us": round(lin, 1),
+            "linear_share": round(lin / span, 3) if span else None,
+            "per_kind_exposed_us": {k: round(v[1], 1) for k, v in sorted(per.items(), key=lambda kv: -kv[1][1])},
+            "how": "device %globaltimer per launch (first CTA entry, last CTA exit) in the replayed graph; "
+                   "exposed = end - max(start, previous launches' end)"}
 
 
 def linear_roofline(model, a, prof: list, batch: int, ctx_mean: float) -> dict:
@@ -514,6 +539,7 @@ def main() -> None:
                   "predicted_speedup_by_gamma_geometric": by_gamma, "predicted_tokens_per_cycle":
                   round(pred.tokens_per_cycle, 3), "acceptance_model": "empirical accept-length distribution of the timed run (device traces)"}
     roof = linear_roofline(model, a, main_q["profile"], a.batch, main_q["ctx_mean"])
+    roof["in_graph"] = critical_path(main_q["ktrace"])
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu:
         cpu = cpu_reference(a, main_q["acceptance_rate"])

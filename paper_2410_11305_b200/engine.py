@@ -197,6 +197,36 @@ class DecodeEngine:
         self._prof_graph = g  # keep alive with its events
         return [(float(ms[i]), int(tags[i])) for i in range(n.value)]
 
+    def ktrace_step(self):
+        """Device timeline of one replayed step with PDL intact (qs_ktrace_*): per traced
+        launch (linears, operand packs, attention) its tag and [first CTA entry, last CTA
+        exit] in microseconds from the step's first entry."""
+        import torch
+        import ctypes as C
+        body = self._cycle_body if self.algorithm == "qspec" else self._ar_body
+        if self.graph is None:
+            self.step()
+        cap = 16384
+        buf = torch.zeros((cap, 2), dtype=torch.int64, device="cuda")
+        _lib.call("qs_ktrace_enable", buf.data_ptr(), cap)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            body()
+        tags = (C.c_int32 * cap)()
+        n = _lib.i32()
+        _lib.call("qs_ktrace_read", C.addressof(tags), cap, C.byref(n))
+        _lib.call("qs_ktrace_enable", None, 0)
+        n = n.value
+        buf[:n, 0] = torch.iinfo(torch.int64).max
+        buf[:n, 1] = 0
+        torch.cuda.synchronize()
+        g.replay()
+        torch.cuda.synchronize()
+        t = buf[:n].cpu().numpy().astype(np.float64)
+        t0 = t[:, 0].min()
+        self._kt_graph = g
+        return [int(tags[i]) for i in range(n)], (t[:, 0] - t0) / 1e3, (t[:, 1] - t0) / 1e3
+
     # ------------------------------------------------------------------ admission
     def prefill(self, slot: int, prompt: list[int], max_new_tokens: int) -> None:
         """specdec.py:234-254: prompt through the HIGH path (greedy_mode for greedy), emit token 1."""
