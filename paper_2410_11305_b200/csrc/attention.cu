@@ -17,7 +17,10 @@
 
 namespace qs {
 
-constexpr int kAttnChunk = 64;
+#ifndef QS_ATTN_CHUNK
+#define QS_ATTN_CHUNK 64
+#endif
+constexpr int kAttnChunk = QS_ATTN_CHUNK;
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");

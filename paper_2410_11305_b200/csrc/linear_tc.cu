@@ -49,9 +49,6 @@
 #ifndef QS_EPI16_TMIN
 #define QS_EPI16_TMIN 32
 #endif
-#ifndef QS_HALF_DEFAULT
-#define QS_HALF_DEFAULT 0
-#endif
 // research ablations (scripts/lin_ablate.sh), 0 in the product build; bit 0: unpack skips
 // LDS + ALU, 1: no MMAs (commits only), 2: epilogue skips TMEM loads + math, 3: unpack
 // skips tcgen05.st, 4: no weight bulk copies (the ring fills without HBM traffic)
@@ -63,50 +60,45 @@ namespace qs {
 
 constexpr size_t kPfPiece = 64 * 1024;  // bytes per cp.async.bulk.prefetch.L2
 
-// H = 1: half-SM configuration for small-T buckets (384 threads, 256 TMEM columns,
-// <= ~100 KB of shared memory, 2 CTAs per SM possible) so the NEXT linear's CTAs can be
-// resident -- and stream their first weight stages -- while this launch's tail drains.
-template <int L, int TMAX, int H = 0>
+template <int L, int TMAX>
 struct LinCfg {
-  static constexpr int kTmemCols = H ? 256 : 512;
   static constexpr int kRowsMax = (L * TMAX) <= 8 ? 8 : ((L * TMAX + 15) / 16) * 16;
   static constexpr int kAccCols = kRowsMax;  // one accumulator block (N columns) per chunk
   // chunks per stage: as many as TMEM allows with 2 acc buffers + 2 A slots
   // (QS_CPS_SMALLN=6 builds 6-chunk stages where TMEM allows: measured neutral)
-  static constexpr int kCPS0 = (QS_CPS_SMALLN == 6 && 2 * 6 * kAccCols + 2 * 6 * 32 <= kTmemCols) ? 6
-                               : (2 * 4 * kAccCols + 2 * 4 * 32 <= kTmemCols) ? 4
-                               : (2 * 2 * kAccCols + 2 * 2 * 32 <= kTmemCols) ? 2 : 1;
+  static constexpr int kCPS0 = (QS_CPS_SMALLN == 6 && 2 * 6 * kAccCols + 2 * 6 * 32 <= 512) ? 6
+                               : (2 * 4 * kAccCols + 2 * 4 * 32 <= 512) ? 4
+                               : (2 * 2 * kAccCols + 2 * 2 * 32 <= 512) ? 2 : 1;
   // wide buckets (N = 192): ONE accumulator buffer of 2-chunk stages instead of two of
   // 1-chunk stages -- half the unpack -> MMA hand-offs per weight byte; the epilogue
   // hands the buffer back right after its tcgen05.ld
-  static constexpr bool kOneAcc = QS_ONE_ACC && kCPS0 == 1 && (2 * kAccCols + 2 * 2 * 32 <= kTmemCols);
+  static constexpr bool kOneAcc = QS_ONE_ACC && kCPS0 == 1 && (2 * kAccCols + 2 * 2 * 32 <= 512);
   static constexpr int kCPS = kOneAcc ? 2 : kCPS0;
   // spend leftover TMEM on deeper rings (lets unpack / epilogue run further ahead)
-  static constexpr int kFree0 = kTmemCols - (kOneAcc ? 1 : 2) * kCPS * kAccCols - 2 * kCPS * 32;
+  static constexpr int kFree0 = 512 - (kOneAcc ? 1 : 2) * kCPS * kAccCols - 2 * kCPS * 32;
   static constexpr int kASlots = 2 + (kFree0 >= kCPS * 32 ? 1 : 0);
   static constexpr int kFree1 = kFree0 - (kASlots - 2) * kCPS * 32;
   static constexpr int kAccBufs =
       kOneAcc ? 1 : 2 + (kFree1 / (kCPS * kAccCols) > 2 ? 2 : kFree1 / (kCPS * kAccCols));
   static constexpr int kAColBase = kAccBufs * kCPS * kAccCols;
+  static constexpr int kTmemCols = 512;
   static_assert(kAColBase + kASlots * kCPS * 32 <= kTmemCols, "TMEM budget");
   static constexpr int kActBytes = kRowsMax * 128;
   static constexpr int kStageBytes = kCPS * (kChunkBytes + kActBytes);
   // 16 warps: 4 control, then unpack and epilogue warps (2 or 1 per TMEM lane
   // quadrant each).  Small T is unpack-bound -> 8 unpack warps; large T is
   // epilogue-bound -> 8 epilogue warps.
-  static constexpr int kUnpackWarps = (TMAX <= QS_UNPACK8_TMAX && !H) ? 8 : 4;
+  static constexpr int kUnpackWarps = TMAX <= QS_UNPACK8_TMAX ? 8 : 4;
   // T >= 32 buckets are epilogue-latency bound (one 3-limb chunk drain + scale-accumulate
   // per stage, only two accumulator buffers fit TMEM): 16 epilogue warps (4 per TMEM lane
   // quadrant, 2 token chunks each) in a 768-thread CTA halve each warp's per-chunk chain
-  static constexpr int kEpiWarps = H ? 4 : (TMAX >= QS_EPI16_TMIN ? 16 : 12 - kUnpackWarps);
-  static constexpr int kMinBlocks = H ? 2 : 1;
-  static constexpr int kSmemBudget = (H ? 96 : 196) * 1024;
+  static constexpr int kEpiWarps = TMAX >= QS_EPI16_TMIN ? 16 : 12 - kUnpackWarps;
   static constexpr int kThreads = 32 * (4 + kUnpackWarps + kEpiWarps);
   static constexpr int kEpiHalves = kEpiWarps / 4;
   static constexpr int kUnpackHalves = kUnpackWarps / 4;
   // residual-emit staging: the tile's new residual rows [T][128] + 1/rms per token
   static constexpr int kStgBytes = (TMAX < 8 ? 8 : TMAX) * 129 * 4;
-  static constexpr int kStages0 = (kSmemBudget - kStgBytes) / kStageBytes;
+  static constexpr int kStages0 = (196 * 1024 - kStgBytes) / kStageBytes;
   // Unpack group g takes the stages i with i % kUnpackHalves == g and waits on
   // wfull[i % kStages] by parity.  kStages must be a multiple of kUnpackHalves so
   // that each weight slot is only ever consumed by ONE group, which then observes
@@ -300,10 +292,9 @@ __device__ __forceinline__ void emit_silu(const LinearArgs& a, int tile, int et,
   if (et == 0) a.e_cnt[8 + q] = 0;
 }
 
-template <int L, int TMAX, int OPC, int H>
-__global__ void __launch_bounds__(LinCfg<L, TMAX, H>::kThreads, LinCfg<L, TMAX, H>::kMinBlocks)
-    linear_tc_kernel(const LinearArgs a) {
-  using C = LinCfg<L, TMAX, H>;
+template <int L, int TMAX, int OPC>
+__global__ void __launch_bounds__(LinCfg<L, TMAX>::kThreads, 1) linear_tc_kernel(const LinearArgs a) {
+  using C = LinCfg<L, TMAX>;
   constexpr int CPS = C::kCPS;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -511,7 +502,7 @@ __global__ void __launch_bounds__(LinCfg<L, TMAX, H>::kThreads, LinCfg<L, TMAX, 
       tc_fence_after();
       if (dbg0 && i < 64 && r == 0) a.dbg[9 * 64 + i] = gtimer();
       // all LDS of the stage first (latency overlap), then unpack + TMEM stores
-      constexpr int kPre = C::kThreads != 512 ? 1 : (CPS <= 4 ? CPS : 1);  // register budget
+      constexpr int kPre = C::kThreads > 512 ? 1 : (CPS <= 4 ? CPS : 1);  // register budget
       uint4 wv[CPS][4];
 #pragma unroll
       for (int q = 0; q < kPre; ++q) {
@@ -609,7 +600,7 @@ __global__ void __launch_bounds__(LinCfg<L, TMAX, H>::kThreads, LinCfg<L, TMAX, 
         constexpr int kCols = C::kTokChunk * L;
         constexpr int KC = kCols <= 8 ? 8 : (kCols <= 16 ? 16 : 24);
         // double-buffer only where the registers allow (no spills under the 128 cap)
-        constexpr bool kPipe = C::kThreads == 512 && 2 * CPS * KC <= 64;
+        constexpr bool kPipe = C::kThreads <= 512 && 2 * CPS * KC <= 64;
         uint32_t rb[kPipe ? 2 : 1][CPS][KC];
         auto issue = [&](int lc, uint32_t (&rr)[CPS][KC]) {
 #pragma unroll
@@ -723,7 +714,7 @@ __global__ void __launch_bounds__(LinCfg<L, TMAX, H>::kThreads, LinCfg<L, TMAX, 
           if (QS_LIN_TIMELINE && a.dbg) a.dbg[5120 + c] = gtimer();
         }
         named_bar(1, kEpiT);
-        constexpr int kPB = C::kThreads != 512 ? 1 : (kOwn <= 1 ? 4 : (kOwn == 2 ? 2 : 1));
+        constexpr int kPB = C::kThreads > 512 ? 1 : (kOwn <= 1 ? 4 : (kOwn == 2 ? 2 : 1));
         for (int cb = c_lo + 1; cb <= c_hi; cb += kPB) {
           float pv[kPB][kOwn * 8];
 #pragma unroll
@@ -866,48 +857,31 @@ __global__ void __launch_bounds__(LinCfg<L, TMAX, H>::kThreads, LinCfg<L, TMAX, 
   ktrace_exit(a.kt);
 }
 
-template <int L, int TMAX, int OPC, int H>
+template <int L, int TMAX, int OPC>
 static cudaError_t launch_linear_op(const LinearArgs& a, cudaStream_t st) {
-  using C = LinCfg<L, TMAX, H>;
+  using C = LinCfg<L, TMAX>;
   static bool attr[kMaxDevices] = {};  // the attribute is per device
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
   if (dev >= kMaxDevices || !attr[dev]) {
-    e = cudaFuncSetAttribute(linear_tc_kernel<L, TMAX, OPC, H>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    e = cudaFuncSetAttribute(linear_tc_kernel<L, TMAX, OPC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              C::kSmemBytes);
     if (e != cudaSuccess) return e;
     if (dev < kMaxDevices) attr[dev] = true;
   }
-  return launch_k(linear_tc_kernel<L, TMAX, OPC, H>, dim3(a.n_cta), dim3(C::kThreads), C::kSmemBytes, st, a);
-}
-
-bool half_sm_linears() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("QS_HALF");
-    v = (e && e[0]) ? (e[0] == '1') : QS_HALF_DEFAULT;
-  }
-  return v == 1;
-}
-
-template <int L, int TMAX, int H>
-static cudaError_t launch_linear_th(const LinearArgs& a, cudaStream_t st) {
-  switch (a.op) {
-    case kOpSiluMul: return launch_linear_op<L, TMAX, kOpSiluMul, H>(a, st);
-    case kOpQkvRope: return launch_linear_op<L, TMAX, kOpQkvRope, H>(a, st);
-    case kOpLogits: return launch_linear_op<L, TMAX, kOpLogits, H>(a, st);
-    default: return launch_linear_op<L, TMAX, kOpStore, H>(a, st);
-  }
+  return launch_k(linear_tc_kernel<L, TMAX, OPC>, dim3(a.n_cta), dim3(C::kThreads), C::kSmemBytes, st, a);
 }
 
 template <int L, int TMAX>
 static cudaError_t launch_linear_t(const LinearArgs& a, cudaStream_t st) {
   if (a.r_pad != LinCfg<L, TMAX>::kRowsMax) return cudaErrorInvalidValue;  // image rows are padded to the bucket
-  if constexpr (TMAX <= 16) {
-    if (half_sm_linears()) return launch_linear_th<L, TMAX, 1>(a, st);
+  switch (a.op) {
+    case kOpSiluMul: return launch_linear_op<L, TMAX, kOpSiluMul>(a, st);
+    case kOpQkvRope: return launch_linear_op<L, TMAX, kOpQkvRope>(a, st);
+    case kOpLogits: return launch_linear_op<L, TMAX, kOpLogits>(a, st);
+    default: return launch_linear_op<L, TMAX, kOpStore>(a, st);
   }
-  return launch_linear_th<L, TMAX, 0>(a, st);
 }
 
 // token buckets; the 3-limb (verify / AR) path adds T <= 2 and T <= 4 (6 / 12 image

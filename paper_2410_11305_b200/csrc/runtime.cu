@@ -183,6 +183,20 @@ PackArgs pack_args(const qs_qweight_t& w, const float* x, int ldx, int T, const 
   return p;
 }
 
+// CTAs of one linear launch: every SM, unless that leaves fewer than QS_MIN_UNITS (tile,
+// chunk) units per CTA -- a small linear (o_proj: 1024 units) spread over 148 CTAs splits
+// each tile 4-5 ways and its stream-K fixups dominate.  Depends only on (N, K), never on
+// T, so the reduction order stays batch-invariant.
+int linear_ctas(int units, int n_tiles) {
+  static int min_units = env_int("QS_MIN_UNITS", 0);
+  int P = units < num_sms() ? units : num_sms();
+  if (min_units > 0 && units / min_units < P) {
+    P = units / min_units;
+    if (P < n_tiles && n_tiles <= num_sms()) P = n_tiles;
+    if (P < 1) P = 1;
+  }
+  return P;
+}
 LinearArgs linear_args(const qs_qweight_t& w, int T, int L, const qs_workspace_t* ws, int op, float* out,
                        int ldo) {
   LinearArgs a{};
@@ -201,7 +215,7 @@ LinearArgs linear_args(const qs_qweight_t& w, int T, int L, const qs_workspace_t
   a.r_pad = img_rows(linear_tmax_bucket(T, L), L);
   a.a_ld = round_up(T, 8);
   const int U = w.n_tiles * w.n_chunks;
-  a.n_cta = U < num_sms() ? U : num_sms();
+  a.n_cta = linear_ctas(U, w.n_tiles);
   a.part = ws->part;
   a.counters = ws->counters;
   a.op = op;
