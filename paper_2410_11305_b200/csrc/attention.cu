@@ -202,7 +202,9 @@ cudaError_t launch_attention(const AttnArgs& a, int n_blk, cudaStream_t st) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
-  if (smem > 48 * 1024 && (dev >= kMaxDevices || smem > attr[dev])) {
+  // static shared memory (ctx_s, row_s) comes on top of the dynamic bytes: opt in above
+  // 47 KB, not at 48 KB exactly (a 32-query block of head_dim 64 is exactly 48 KB dynamic)
+  if (smem > 47 * 1024 && (dev >= kMaxDevices || smem > attr[dev])) {
     e = cudaFuncSetAttribute(attn_partial_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     if (dev < kMaxDevices) attr[dev] = smem;

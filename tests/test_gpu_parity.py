@@ -183,6 +183,20 @@ def test_forward_batched_equals_chained():
         assert torch.equal(kv_a.rows(li, 0, 5, "v"), kv_b.rows(li, 0, 5, "v"))
 
 
+@pytest.mark.parametrize("T", [16, 32, 48, 64])
+def test_prefill_blocks_of_every_size(T):
+    # head_dim 64 with a 32-query block is exactly 48 KB of dynamic attention smem (plus
+    # the static bytes): the launch must opt in above the default limit
+    from paper_2410_11305_b200.model import run_forward_chunks
+    m = Q.random_init(Q.ModelConfig(**TINY), 0)
+    ids = [int(t) for t in np.random.default_rng(T).integers(0, 1024, T)]
+    kv_a, kv_b = Q.KVCache(m.config), Q.KVCache(m.config)
+    la, aa = run_forward_chunks(m, kv_a, ids, 0, False)
+    rows = [run_forward_chunks(m, kv_b, [t], i, False) for i, t in enumerate(ids)]
+    assert np.array_equal(aa.cpu().numpy(), np.concatenate([r[1].cpu().numpy() for r in rows]))
+    assert np.array_equal(la.cpu().numpy(), np.concatenate([r[0].cpu().numpy() for r in rows]))
+
+
 def test_tiny_greedy_and_qspec_tokens(golden):
     m = Q.random_init(Q.ModelConfig(**TINY), 0)
     prompts = golden["tiny.prompts"]
