@@ -49,6 +49,9 @@
 #ifndef QS_EPI16_TMIN
 #define QS_EPI16_TMIN 32
 #endif
+#ifndef QS_U8E8_T
+#define QS_U8E8_T 0
+#endif
 // research ablations (scripts/lin_ablate.sh), 0 in the product build; bit 0: unpack skips
 // LDS + ALU, 1: no MMAs (commits only), 2: epilogue skips TMEM loads + math, 3: unpack
 // skips tcgen05.st, 4: no weight bulk copies (the ring fills without HBM traffic)
@@ -88,11 +91,13 @@ struct LinCfg {
   // 16 warps: 4 control, then unpack and epilogue warps (2 or 1 per TMEM lane
   // quadrant each).  Small T is unpack-bound -> 8 unpack warps; large T is
   // epilogue-bound -> 8 epilogue warps.
-  static constexpr int kUnpackWarps = TMAX <= QS_UNPACK8_TMAX ? 8 : 4;
+  // QS_U8E8_T: buckets of exactly this T get 8 unpack AND 8 epilogue warps (640 threads)
+  static constexpr bool kU8E8 = TMAX == QS_U8E8_T;
+  static constexpr int kUnpackWarps = (TMAX <= QS_UNPACK8_TMAX || kU8E8) ? 8 : 4;
   // T >= 32 buckets are epilogue-latency bound (one 3-limb chunk drain + scale-accumulate
   // per stage, only two accumulator buffers fit TMEM): 16 epilogue warps (4 per TMEM lane
   // quadrant, 2 token chunks each) in a 768-thread CTA halve each warp's per-chunk chain
-  static constexpr int kEpiWarps = TMAX >= QS_EPI16_TMIN ? 16 : 12 - kUnpackWarps;
+  static constexpr int kEpiWarps = TMAX >= QS_EPI16_TMIN ? 16 : (kU8E8 ? 8 : 12 - kUnpackWarps);
   static constexpr int kThreads = 32 * (4 + kUnpackWarps + kEpiWarps);
   static constexpr int kEpiHalves = kEpiWarps / 4;
   static constexpr int kUnpackHalves = kUnpackWarps / 4;
@@ -502,7 +507,7 @@ __global__ void __launch_bounds__(LinCfg<L, TMAX>::kThreads, 1) linear_tc_kernel
       tc_fence_after();
       if (dbg0 && i < 64 && r == 0) a.dbg[9 * 64 + i] = gtimer();
       // all LDS of the stage first (latency overlap), then unpack + TMEM stores
-      constexpr int kPre = C::kThreads > 512 ? 1 : (CPS <= 4 ? CPS : 1);  // register budget
+      constexpr int kPre = C::kThreads > 640 ? 1 : (C::kThreads > 512 ? 2 : (CPS <= 4 ? CPS : 1));  // register budget
       uint4 wv[CPS][4];
 #pragma unroll
       for (int q = 0; q < kPre; ++q) {
