@@ -28,6 +28,8 @@
 //               deterministic), fused post-op.
 // The reduction order of every output depends only on (N, K, grid), never on T,
 // so an n-token call is bit-identical to n single-token calls.
+#include <type_traits>
+
 #include "pack_dev.cuh"
 
 // per-stage globaltimer stamps for scripts/linear_timeline.py (build with
@@ -200,6 +202,7 @@ struct StageIt {
 // covers store / residual / dump (runtime a.op), every other class is exact.
 template <int OPC, int O>
 __device__ __forceinline__ bool op_is(const LinearArgs& a) {
+  if constexpr (OPC == kOpAny) return O != kOpDump && a.op == O;  // chains: never a dump
   constexpr bool in_class = OPC == kOpStore ? (O == kOpStore || O == kOpResidual || O == kOpDump) : O == OPC;
   if constexpr (!in_class) return false;
   if constexpr (OPC != kOpStore) return true;
@@ -212,9 +215,22 @@ __device__ __forceinline__ bool op_is(const LinearArgs& a) {
 // splits down to 128-element leaves, each summed with 8 strided accumulators and the
 // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) bracket; leaves combine as a balanced tree
 // (token_inv_rms in pack_dev.cuh states the same order).
-template <int L, int kEpiT, int kEpiWarps>
-__device__ __forceinline__ void emit_rms(const LinearArgs& a, float* stg, int tile, int et) {
+// Chain launches (kSignal): after quantising, publish the chunk on *sig (release) for the
+// next linear's operand wait.
+template <int kEpiT, bool kSignal>
+__device__ __forceinline__ void emit_publish(int* sig, int et) {
+  if constexpr (kSignal) {
+    if (sig == nullptr) return;
+    named_bar(1, kEpiT);  // the CTA's chunk writes, then one cumulative gpu-scope release
+    if (et == 0) red_release_add(sig, 1);
+  }
+}
+template <int L, int TMAX, int kEpiT, int kEpiWarps, bool kSignal>
+__device__ __forceinline__ void emit_rms(const LinearArgs& a, float* stg, int tile, int et, int* sig) {
   const int lane = et & 31, ew = et >> 5;
+  constexpr int kTW = (TMAX + kEpiWarps - 1) / kEpiWarps;  // tokens per warp
+  // this tile's RMSNorm weights do not depend on the barrier: in flight across it
+  const float4 wv = *reinterpret_cast<const float4*>(a.e_rms_w + (size_t)tile * 128 + 4 * lane);
   named_bar(1, kEpiT);
   for (int base = 0; base < a.T * 8; base += kEpiT) {
     const int item = base + et, t = item >> 3, j = item & 7;
@@ -231,7 +247,7 @@ __device__ __forceinline__ void emit_rms(const LinearArgs& a, float* stg, int ti
     rs = __fadd_rn(rs, __shfl_xor_sync(0xffffffffu, rs, 4));
     if (on && j == 0) __stcg(a.e_leaf + (size_t)t * a.n_tiles + tile, rs);
   }
-  __threadfence();
+  // bar.sync then ONE gpu-scope release by et 0: cumulative over the CTA's leaf writes
   named_bar(1, kEpiT);
   if (et == 0) {
     red_release_add(&a.e_cnt[0], 1);
@@ -243,17 +259,26 @@ __device__ __forceinline__ void emit_rms(const LinearArgs& a, float* stg, int ti
   named_bar(1, kEpiT);
   float* inv = stg + 128 * (a.T > 8 ? a.T : 8);
   const int nl = a.n_tiles, per = nl > 32 ? nl >> 5 : 1, lanes = nl > 32 ? 32 : nl;
-  for (int t = ew; t < a.T; t += kEpiWarps) {
-    const float* lf = a.e_leaf + (size_t)t * nl;
-    float s[4];
+  // every leaf load of this warp's tokens in flight at once, then the pairwise sums
+  float s[kTW][4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) s[i] = (i < per && lane * per + i < nl) ? __ldcg(lf + lane * per + i) : 0.f;
-    if (per >= 2) s[0] = __fadd_rn(s[0], s[1]);
+  for (int k = 0; k < kTW; ++k) {
+    const int t = ew + k * kEpiWarps;
+    const float* lf = a.e_leaf + (size_t)t * nl;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      s[k][i] = (t < a.T && i < per && lane * per + i < nl) ? __ldcg(lf + lane * per + i) : 0.f;
+  }
+#pragma unroll
+  for (int k = 0; k < kTW; ++k) {
+    const int t = ew + k * kEpiWarps;
+    if (t >= a.T) break;
+    if (per >= 2) s[k][0] = __fadd_rn(s[k][0], s[k][1]);
     if (per >= 4) {
-      s[2] = __fadd_rn(s[2], s[3]);
-      s[0] = __fadd_rn(s[0], s[2]);
+      s[k][2] = __fadd_rn(s[k][2], s[k][3]);
+      s[k][0] = __fadd_rn(s[k][0], s[k][2]);
     }
-    float v = s[0];
+    float v = s[k][0];
     for (int off = 1; off < lanes; off <<= 1) v = __fadd_rn(v, __shfl_xor_sync(0xffffffffu, v, off));
     if (lane == 0) {
       const float ms = __fdiv_rn(v, (float)a.e_n);
@@ -267,38 +292,59 @@ __device__ __forceinline__ void emit_rms(const LinearArgs& a, float* stg, int ti
       a.e_cnt[1] = 0;
     }
   }
-  for (int t = ew; t < a.T; t += kEpiWarps) {
+#pragma unroll
+  for (int k = 0; k < kTW; ++k) {
+    const int t = ew + k * kEpiWarps;
+    if (t >= a.T) break;
     const float iv = inv[t];
     const float4 xv = *reinterpret_cast<const float4*>(stg + t * 128 + 4 * lane);
-    const float4 wv = *reinterpret_cast<const float4*>(a.e_rms_w + (size_t)tile * 128 + 4 * lane);
     const float v[4] = {__fmul_rn(__fmul_rn(xv.x, iv), wv.x), __fmul_rn(__fmul_rn(xv.y, iv), wv.y),
                         __fmul_rn(__fmul_rn(xv.z, iv), wv.z), __fmul_rn(__fmul_rn(xv.w, iv), wv.w)};
     quant_group_warp<L>(v, t, tile, lane, a.e_img, a.e_ascale, a.e_acorr, a.r_pad, a.a_ld, a.e_rotate != 0);
   }
+  emit_publish<kEpiT, kSignal>(sig, et);
 }
 
 // kEmitSilu (gate_up): tiles 2q, 2q+1 hold silu outputs 128q..128q+127 = group q of
 // down_proj's input.  Each owner publishes its half; the second one quantises the group.
-template <int L, int kEpiT, int kEpiWarps>
-__device__ __forceinline__ void emit_silu(const LinearArgs& a, int tile, int et, int* flag) {
+template <int L, int TMAX, int kEpiT, int kEpiWarps, bool kSignal>
+__device__ __forceinline__ void emit_silu(const LinearArgs& a, int tile, int et, int* flag, int* sig) {
+  constexpr int kTW = (TMAX + kEpiWarps - 1) / kEpiWarps;  // tokens per warp
   const int lane = et & 31, ew = et >> 5, q = tile >> 1;
-  __threadfence();
-  named_bar(1, kEpiT);
+  named_bar(1, kEpiT);  // the CTA's h writes, then et 0's acq_rel add (cumulative release)
   if (et == 0) *flag = atom_add_acq_rel(&a.e_cnt[8 + q], 1);
   named_bar(1, kEpiT);
   const int second = *flag;
   named_bar(1, kEpiT);
   if (second != 1) return;
-  for (int t = ew; t < a.T; t += kEpiWarps) {
-    const float4 hv = __ldcg(reinterpret_cast<const float4*>(a.out + (size_t)t * a.ldo + 128 * q) + lane);
-    const float v[4] = {hv.x, hv.y, hv.z, hv.w};
+  float4 hv[kTW];  // all of this warp's rows in flight at once
+#pragma unroll
+  for (int k = 0; k < kTW; ++k) {
+    const int t = ew + k * kEpiWarps;
+    hv[k] = t < a.T ? __ldcg(reinterpret_cast<const float4*>(a.out + (size_t)t * a.ldo + 128 * q) + lane)
+                    : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+#pragma unroll
+  for (int k = 0; k < kTW; ++k) {
+    const int t = ew + k * kEpiWarps;
+    if (t >= a.T) break;
+    const float v[4] = {hv[k].x, hv[k].y, hv[k].z, hv[k].w};
     quant_group_warp<L>(v, t, q, lane, a.e_img, a.e_ascale, a.e_acorr, a.r_pad, a.a_ld, a.e_rotate != 0);
   }
   if (et == 0) a.e_cnt[8 + q] = 0;
+  emit_publish<kEpiT, kSignal>(sig, et);
 }
 
-template <int L, int TMAX, int OPC>
-__global__ void __launch_bounds__(LinCfg<L, TMAX>::kThreads, 1) linear_tc_kernel(const LinearArgs a) {
+// The linear kernel body.  A single launch runs one linear (A = its argument block,
+// nlin = 1); a chain launch (CHAIN, OPC = kOpAny) runs the nlin linears of a
+// LinearChain back to back in one persistent grid: every role walks the chain's
+// linears in order with its ring positions carried across them, so linear j+1's weight
+// stream starts as soon as the ring has room while linear j's fixups and operand emit
+// are still running.  Only linear j+1's activation copies (warp 2 images, warp 3
+// scales) and its epilogue wait for ready[j+1] (every operand chunk emitted).
+template <int L, int TMAX, int OPC, bool CHAIN>
+__device__ __forceinline__ void linear_body(const LinearArgs* __restrict__ A, const int nlin, int* ready,
+                                            int* exit_cnt) {
   using C = LinCfg<L, TMAX>;
   constexpr int CPS = C::kCPS;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -320,12 +366,10 @@ __global__ void __launch_bounds__(LinCfg<L, TMAX>::kThreads, 1) linear_tc_kernel
   int* red_idx = reinterpret_cast<int*>(red_val + 4 * TMAX);  // [4][TMAX]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int NC = a.n_chunks;
-  const int U = a.n_tiles * NC, P = a.n_cta, c = blockIdx.x;
-  const int u0 = unit_bound(c, U, P), u1 = unit_bound(c + 1, U, P);
-  const bool dbg0 = QS_LIN_TIMELINE && a.dbg != nullptr && c == 0;
-  if (QS_LIN_TIMELINE && a.dbg && threadIdx.x == 0) a.dbg[1024 + c] = gtimer();
-  ktrace_enter(a.kt);
+  const int c = blockIdx.x;
+  const bool dbg0 = QS_LIN_TIMELINE && A[0].dbg != nullptr && c == 0;
+  if (QS_LIN_TIMELINE && A[0].dbg && threadIdx.x == 0) A[0].dbg[1024 + c] = gtimer();
+  ktrace_enter(A[0].kt);
   pdl_launch_dependents();
 
   if (threadIdx.x == 0) {
@@ -350,14 +394,115 @@ __global__ void __launch_bounds__(LinCfg<L, TMAX>::kThreads, 1) linear_tc_kernel
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t act_bytes = (uint32_t)a.r_pad * 128u;
+  // per-linear geometry (the chain's linears share T, L and so r_pad; every CTA of a
+  // chain launch holds units of every linear: host checks n_cta == grid)
+#define QS_LIN_GEOM(j)                                   \
+  const LinearArgs& a = A[j];                            \
+  const int NC = a.n_chunks;                             \
+  const int U = a.n_tiles * NC, P = a.n_cta;             \
+  const int u0 = unit_bound(c, U, P), u1 = unit_bound(c + 1, U, P); \
+  (void)u0;                                              \
+  (void)u1;
+  // spin (all lanes) until linear j's operand is complete, then order the async-proxy
+  // (bulk copy) reads after the generic-proxy writes of the emitting CTAs
+  auto wait_operand = [&](int j) {
+    const unsigned long long t0 = gtimer();
+    while (ld_acquire(ready + j) < A[j].n_chunks) {
+      if (gtimer() - t0 > 5000000000ull) __trap();
+    }
+    fence_proxy_async_global();
+  };
+  (void)wait_operand;
 
-  if (warp == 0) {
+  if (CHAIN && warp == 0) {
+    // ------------------------------------------------------------ weight producer (chain)
+    int i = 0;  // ring position, carried across the chain's linears
+    for (int j = 0; j < nlin; ++j) {
+      QS_LIN_GEOM(j)
+      if (lane == 0 && a.pf_n > 0) {  // this CTA's share of the look-ahead window
+        size_t tot = 0;
+        for (int r = 0; r < a.pf_n; ++r) tot += a.pf_len[r];
+        size_t lo = (tot * (size_t)c / P) & ~(size_t)15, hi = (tot * (size_t)(c + 1) / P) & ~(size_t)15;
+        if (c == P - 1) hi = tot;
+        size_t base = 0;
+        for (int r = 0; r < a.pf_n && lo < hi; ++r) {
+          const size_t e = base + a.pf_len[r];
+          if (lo < e) {
+            const size_t x0 = lo - base, x1 = (hi < e ? hi : e) - base;
+            for (size_t o = x0; o < x1; o += kPfPiece)
+              prefetch_l2(a.pf_ptr[r] + o, (uint32_t)(x1 - o < kPfPiece ? x1 - o : kPfPiece));
+            lo = base + x1;
+          }
+          base = e;
+        }
+      }
+      __syncwarp();
+      StageIt it{u0, u1, NC, CPS};
+      for (; it.next(); ++i) {
+        const int s = i % C::kStages;
+        mbar_wait(&empty[s], ((i / C::kStages) & 1) ^ 1);  // fresh slots: parity 1 passes
+        mbar_arrive_expect_tx_elect(&wfull[s], (uint32_t)it.nq * kChunkBytes);
+        bulk_g2s_elect(smem + s * C::kStageBytes, a.codes + ((size_t)it.tile * NC + it.ch0) * kChunkBytes,
+                       it.nq * kChunkBytes, &wfull[s]);
+      }
+    }
+  } else if (CHAIN && warp == 2) {
+    // ------------------------------------------------------------ activation-image producer (chain)
+    pdl_wait();
+    int i = 0;
+    for (int j = 0; j < nlin; ++j) {
+      QS_LIN_GEOM(j)
+      const uint32_t act_bytes = (uint32_t)a.r_pad * 128u;
+      if (j > 0) wait_operand(j);
+      StageIt it{u0, u1, NC, CPS};
+      for (; it.next(); ++i) {
+        const int s = i % C::kStages;
+        mbar_wait(&empty[s], ((i / C::kStages) & 1) ^ 1);
+        mbar_arrive_expect_tx_elect(&afull[s], (uint32_t)it.nq * act_bytes);
+        bulk_g2s_elect(smem + s * C::kStageBytes + CPS * kChunkBytes, a.act + (size_t)it.ch0 * act_bytes,
+                       it.nq * act_bytes, &afull[s]);
+      }
+    }
+  } else if (CHAIN && warp == 3) {
+    // ------------------------------------------------------------ scale producer (chain)
+    // weight scales of up to kSStages entries go out before the operand wait, the
+    // activation scales / correction sums of those entries after it
+    int i = 0;
+    for (int j = 0; j < nlin; ++j) {
+      QS_LIN_GEOM(j)
+      const uint32_t a_bytes = (uint32_t)a.a_ld * 4u;
+      const uint32_t e_bytes = 512u + (C::kUns ? 5u : 1u) * a_bytes;
+      auto act_part = [&](const StageIt& st, int ss) {
+        float* se = sring + ss * (C::kSEntry / 4);
+        bulk_g2s_elect(se + CPS * 128, a.ascale + (size_t)st.ch0 * a.a_ld, st.nq * a_bytes, &sfull[ss]);
+        if (C::kUns)
+          bulk_g2s_elect(se + C::kCorrOff, a.acorr + (size_t)st.ch0 * a.a_ld * 4, st.nq * 4u * a_bytes, &sfull[ss]);
+      };
+      auto w_part = [&](const StageIt& st, int ss) {
+        mbar_wait(&sempty[ss], ((i / C::kSStages) & 1) ^ 1);
+        mbar_arrive_expect_tx_elect(&sfull[ss], (uint32_t)st.nq * e_bytes);
+        bulk_g2s_elect(sring + ss * (C::kSEntry / 4), a.wscale + ((size_t)st.tile * NC + st.ch0) * kTileN,
+                       st.nq * 512u, &sfull[ss]);
+      };
+      StageIt it{u0, u1, NC, CPS}, ia{u0, u1, NC, CPS};
+      const int i0 = i;
+      int npro = 0;
+      for (; npro < C::kSStages && it.next(); ++npro, ++i) w_part(it, i % C::kSStages);
+      if (j == 0) pdl_wait(); else wait_operand(j);
+      for (int k = 0; k < npro && ia.next(); ++k) act_part(ia, (i0 + k) % C::kSStages);
+      for (; it.next(); ++i) {
+        w_part(it, i % C::kSStages);
+        act_part(it, i % C::kSStages);
+      }
+    }
+  } else if (!CHAIN && warp == 0) {
     // ------------------------------------------------------------ weight/act producer (warp-wide, elected issue)
     // Weights do not depend on the previous kernel: the first kStages stages of
     // weights are requested before griddepcontrol.wait (PDL overlap); activation
     // images only after it.
     {
+      QS_LIN_GEOM(0)
+      const uint32_t act_bytes = (uint32_t)a.r_pad * 128u;
       StageIt it{u0, u1, NC, CPS};
       int npro = 0;
       for (; npro < C::kStages && it.next(); ++npro) {
@@ -425,12 +570,13 @@ __global__ void __launch_bounds__(LinCfg<L, TMAX>::kThreads, 1) linear_tc_kernel
         if (dbg0 && i < 64 && lane == 0) a.dbg[0 * 64 + i] = gtimer();
       }
     }
-  } else if (warp == 3) {
+  } else if (!CHAIN && warp == 3) {
     // ------------------------------------------------------------ scale producer (warp-wide, elected issue)
     // Weight scales do not depend on the previous kernel: the first kSStages entries'
     // weight scales are requested before griddepcontrol.wait (with the whole entry's
     // byte count expected up front), the activation scales / correction sums after it.
     {
+      QS_LIN_GEOM(0)
       const uint32_t a_bytes = (uint32_t)a.a_ld * 4u;
       const uint32_t e_bytes = 512u + (C::kUns ? 5u : 1u) * a_bytes;  // per chunk
       auto act_part = [&](float* se, const StageIt& st, int ss) {
@@ -459,10 +605,12 @@ __global__ void __launch_bounds__(LinCfg<L, TMAX>::kThreads, 1) linear_tc_kernel
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer (warp-wide, elected issue)
-    {
+    int i = 0;
+    for (int j = 0; j < nlin; ++j) {
+      QS_LIN_GEOM(j)
       const uint32_t idesc = idesc_i8(128, (uint32_t)a.r_pad, !C::kUns);
       StageIt it{u0, u1, NC, CPS};
-      for (int i = 0; it.next(); ++i) {
+      for (; it.next(); ++i) {
         const int s = i % C::kStages, b = i % C::kAccBufs, as_ = i % C::kASlots;
         if (dbg0 && i < 64 && lane == 0) a.dbg[4 * 64 + i] = gtimer();
         mbar_wait(&accempty[b], ((i / C::kAccBufs) & 1) ^ 1);
@@ -497,8 +645,11 @@ __global__ void __launch_bounds__(LinCfg<L, TMAX>::kThreads, 1) linear_tc_kernel
     // latency chains (LDS -> ALU -> tcgen05.st -> wait) overlap.
     const int q4 = warp & 3, ug = (warp - 4) >> 2, r = q4 * 32 + lane;
     const uint32_t lane_base = (uint32_t)(q4 * 32) << 16;
+    int i = 0;
+    for (int j = 0; j < nlin; ++j) {
+    QS_LIN_GEOM(j)
     StageIt it{u0, u1, NC, CPS};
-    for (int i = 0; it.next(); ++i) {
+    for (; it.next(); ++i) {
       if ((i % C::kUnpackHalves) != ug) continue;
       const int s = i % C::kStages, b = i % C::kASlots;
       mbar_wait_warp(&wfull[s], (i / C::kStages) & 1, 0);
@@ -554,6 +705,7 @@ __global__ void __launch_bounds__(LinCfg<L, TMAX>::kThreads, 1) linear_tc_kernel
       if (lane == 0) mbar_arrive(&tfull[b]);
       if (dbg0 && i < 64 && r == 0) a.dbg[1 * 64 + i] = gtimer();
     }
+    }
   } else if (warp >= 4 + C::kUnpackWarps) {
     // ------------------------------------------------------------ epilogue
     // lane quadrant q4 = warp & 3 (TMEM lanes 32q4.. = tile rows); half h owns the
@@ -567,8 +719,20 @@ __global__ void __launch_bounds__(LinCfg<L, TMAX>::kThreads, 1) linear_tc_kernel
     float acc[kOwn * 8];
 #pragma unroll
     for (int t = 0; t < kOwn * 8; ++t) acc[t] = 0.f;
+    int i = 0;
+    for (int j = 0; j < nlin; ++j) {
+    QS_LIN_GEOM(j)
+    if (CHAIN && j > 0) {  // the residual rows / h this linear reads were written by earlier ones
+      if (et == 0) {
+        const unsigned long long t0 = gtimer();
+        while (ld_acquire(ready + j) < a.n_chunks) {
+          if (gtimer() - t0 > 5000000000ull) __trap();
+        }
+      }
+      named_bar(1, kEpiT);
+    }
     StageIt it{u0, u1, NC, CPS};
-    for (int i = 0; it.next(); ++i) {
+    for (; it.next(); ++i) {
       const int b = i % C::kAccBufs, ss = i % C::kSStages;
       const int tile = it.tile, n = tile * kTileN + r;
       mbar_wait_warp(&sfull[ss], (i / C::kSStages) & 1, 0);
@@ -741,126 +905,195 @@ __global__ void __launch_bounds__(LinCfg<L, TMAX>::kThreads, 1) linear_tc_kernel
         }
       }
       // ---------------------------------------------------------- post-ops
-      const bool valid = n < a.n;
-#pragma unroll
-      for (int lc = 0; lc < kOwn; ++lc) {
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const int t = (kH * lc + h) * 8 + e;
-          const float v = acc[lc * 8 + e];
-          if (op_is<OPC, kOpStore>(a) || op_is<OPC, kOpResidual>(a)) {
-            if (t < a.T && valid) {
-              float* o = a.out + (size_t)t * a.ldo + n;
-              const float nv = (op_is<OPC, kOpResidual>(a)) ? __fadd_rn(*o, v) : v;
-              *o = nv;
-              if (OPC == kOpStore && a.emit == kEmitRms) reinterpret_cast<float*>(smem + C::kStgOff)[t * 128 + r] = nv;
+      // one specialised tail per post-op class; a chain (OPC = kOpAny) dispatches once per tile
+      auto post = [&](auto opc) {
+        constexpr int OP = decltype(opc)::value;
+        const bool valid = n < a.n;
+        // Every load of the tail is issued before its first store (a load behind a store
+        // to a may-alias pointer would wait a full L2 round trip per element).
+        float pre[kOwn * 8];  // store class: residual rows
+        if constexpr (OP == kOpStore) {
+          const bool res = op_is<OP, kOpResidual>(a);
+  #pragma unroll
+          for (int k = 0; k < kOwn * 8; ++k) {
+            const int t = (kH * (k >> 3) + h) * 8 + (k & 7);
+            pre[k] = (res && t < a.T && valid) ? __ldcg(a.out + (size_t)t * a.ldo + n) : 0.f;
+          }
+        }
+  #pragma unroll
+        for (int lc = 0; lc < kOwn; ++lc) {
+          float pc[8], ps[8];  // qkv: cos / sin of the chunk's 8 tokens
+          int pr[8];           // qkv: KV page * page_len + in-page row
+          if constexpr (OP == kOpQkvRope) {
+            const bool is_v = n >= a.n_q + a.n_k;
+            const int loc = n < a.n_q ? n : (is_v ? n - a.n_q - a.n_k : n - a.n_q);
+            const int half = a.hd >> 1, ip = (loc % a.hd) >> 1;
+  #pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const int t = (kH * lc + h) * 8 + e;
+              pr[e] = (t < a.T) ? a.pos[t] : 0;  // position (uniform per warp)
             }
-          } else if (op_is<OPC, kOpSiluMul>(a)) {
-            const float other = __shfl_xor_sync(0xffffffffu, v, 1);
-            if (t < a.T && valid && (r & 1) == 0)
-              a.out[(size_t)t * a.ldo + (n >> 1)] = __fmul_rn(silu_ref(v), other);
-          } else if (op_is<OPC, kOpQkvRope>(a)) {
-            const float other = __shfl_xor_sync(0xffffffffu, v, 1);
-            if (t < a.T && valid) {
-              const bool is_v = n >= a.n_q + a.n_k;
-              const int loc = n < a.n_q ? n : (is_v ? n - a.n_q - a.n_k : n - a.n_q);
-              const int d = loc % a.hd, head = loc / a.hd, half = a.hd >> 1, ip = d >> 1;
-              const bool odd = (d & 1) != 0;
-              const int p = a.pos[t];
-              float val = v;
-              if (!is_v) {
-                // model.py:243-252: even' = e*c - o*s ; odd' = e*s + o*c
-                const float cs = a.rope_cos[(size_t)p * half + ip], sn = a.rope_sin[(size_t)p * half + ip];
-                const float ev = odd ? other : v, ov = odd ? v : other;
-                val = odd ? __fadd_rn(__fmul_rn(ev, sn), __fmul_rn(ov, cs))
-                          : __fsub_rn(__fmul_rn(ev, cs), __fmul_rn(ov, sn));
-              }
-              if (n < a.n_q) {
-                a.out[(size_t)t * a.ldo + n] = val;
-              } else {
-                const int sl = a.slot[t];
-                const int pg = a.block_table[(size_t)sl * a.bt_ld + p / a.page];
-                const size_t off = (((size_t)pg * a.n_kv_heads + head) * a.page + (p % a.page)) * a.hd + d;
-                (is_v ? a.vcache : a.kcache)[off] = val;
-              }
+  #pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const int t = (kH * lc + h) * 8 + e;
+              const bool on = t < a.T && valid;
+              const int p = pr[e];
+              pc[e] = (on && !is_v) ? a.rope_cos[(size_t)p * half + ip] : 0.f;
+              ps[e] = (on && !is_v) ? a.rope_sin[(size_t)p * half + ip] : 0.f;
+              pr[e] = (on && n >= a.n_q) ? a.block_table[(size_t)a.slot[t] * a.bt_ld + p / a.page] * a.page + p % a.page
+                                         : 0;
             }
-          } else if (op_is<OPC, kOpLogits>(a)) {
-            if (t < a.T) {
-              if (a.out != nullptr && valid) a.out[(size_t)t * a.ldo + n] = v;
-              float bv = valid ? v : -INFINITY;
-              int bi = valid ? n : 0x7fffffff;
-#pragma unroll
-              for (int off = 16; off > 0; off >>= 1) {
-                const float ov = __shfl_xor_sync(0xffffffffu, bv, off);
-                const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
-                if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+          }
+  #pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const int t = (kH * lc + h) * 8 + e;
+            const float v = acc[lc * 8 + e];
+            if (op_is<OP, kOpStore>(a) || op_is<OP, kOpResidual>(a)) {
+              if (t < a.T && valid) {
+                const float nv = (op_is<OP, kOpResidual>(a)) ? __fadd_rn(pre[lc * 8 + e], v) : v;
+                a.out[(size_t)t * a.ldo + n] = nv;
+                if (OP == kOpStore && a.emit == kEmitRms)
+                  reinterpret_cast<float*>(smem + C::kStgOff)[t * 128 + r] = nv;
               }
-              if (lane == 0) { red_val[q4 * TMAX + t] = bv; red_idx[q4 * TMAX + t] = bi; }
+            } else if (op_is<OP, kOpSiluMul>(a)) {
+              const float other = __shfl_xor_sync(0xffffffffu, v, 1);
+              if (t < a.T && valid && (r & 1) == 0)
+                a.out[(size_t)t * a.ldo + (n >> 1)] = __fmul_rn(silu_ref(v), other);
+            } else if (op_is<OP, kOpQkvRope>(a)) {
+              const float other = __shfl_xor_sync(0xffffffffu, v, 1);
+              if (t < a.T && valid) {
+                const bool is_v = n >= a.n_q + a.n_k;
+                const int loc = n < a.n_q ? n : (is_v ? n - a.n_q - a.n_k : n - a.n_q);
+                const int d = loc % a.hd, head = loc / a.hd;
+                const bool odd = (d & 1) != 0;
+                float val = v;
+                if (!is_v) {
+                  // model.py:243-252: even' = e*c - o*s ; odd' = e*s + o*c
+                  const float cs = pc[e], sn = ps[e];
+                  const float ev = odd ? other : v, ov = odd ? v : other;
+                  val = odd ? __fadd_rn(__fmul_rn(ev, sn), __fmul_rn(ov, cs))
+                            : __fsub_rn(__fmul_rn(ev, cs), __fmul_rn(ov, sn));
+                }
+                if (n < a.n_q) {
+                  a.out[(size_t)t * a.ldo + n] = val;
+                } else {
+                  const int pg = pr[e] / a.page, row = pr[e] - pg * a.page;
+                  const size_t off = (((size_t)pg * a.n_kv_heads + head) * a.page + row) * a.hd + d;
+                  (is_v ? a.vcache : a.kcache)[off] = val;
+                }
+              }
+            } else if (op_is<OP, kOpLogits>(a)) {
+              if (t < a.T) {
+                if (a.out != nullptr && valid) a.out[(size_t)t * a.ldo + n] = v;
+                float bv = valid ? v : -INFINITY;
+                int bi = valid ? n : 0x7fffffff;
+  #pragma unroll
+                for (int off = 16; off > 0; off >>= 1) {
+                  const float ov = __shfl_xor_sync(0xffffffffu, bv, off);
+                  const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+                  if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+                }
+                if (lane == 0) { red_val[q4 * TMAX + t] = bv; red_idx[q4 * TMAX + t] = bi; }
+              }
             }
           }
         }
-      }
-      if (op_is<OPC, kOpLogits>(a)) {
-        named_bar(1, kEpiT);
-        if (et < a.T) {
-          float bv = red_val[et];
-          int bi = red_idx[et];
-          for (int w = 1; w < 4; ++w) {
-            const float ov = red_val[w * TMAX + et];
-            const int oi = red_idx[w * TMAX + et];
-            if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
-          }
-          a.arg_val[(size_t)tile * TMAX + et] = bv;
-          a.arg_idx[(size_t)tile * TMAX + et] = bi;
-        }
-        __threadfence();
-        named_bar(1, kEpiT);
-        if (et == 0) {
-          const int old = atomicAdd(&a.counters[a.n_tiles], 1);
-          *flag = (old == a.n_tiles - 1);
-        }
-        named_bar(1, kEpiT);
-        const int last = *flag;
-        named_bar(1, kEpiT);
-        if (last) {
-          __threadfence();
+        if (op_is<OP, kOpLogits>(a)) {
+          named_bar(1, kEpiT);
           if (et < a.T) {
-            const volatile float* av = a.arg_val;
-            const volatile int* ai = a.arg_idx;
-            float bv = av[et];
-            int bi = ai[et];
-            for (int tt = 1; tt < a.n_tiles; ++tt) {
-              const float ov = av[(size_t)tt * TMAX + et];
-              const int oi = ai[(size_t)tt * TMAX + et];
+            float bv = red_val[et];
+            int bi = red_idx[et];
+            for (int w = 1; w < 4; ++w) {
+              const float ov = red_val[w * TMAX + et];
+              const int oi = red_idx[w * TMAX + et];
               if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
             }
-            if (a.arg_rec != nullptr)
-              a.arg_rec[et] = make_int2(__float_as_int(bv), bi + a.arg_off);
-            else
-              a.argmax_out[et] = bi;
+            a.arg_val[(size_t)tile * TMAX + et] = bv;
+            a.arg_idx[(size_t)tile * TMAX + et] = bi;
           }
-          if (et == 0) a.counters[a.n_tiles] = 0;
+          named_bar(1, kEpiT);
+          if (et == 0) {
+            const int old = atom_add_acq_rel(&a.counters[a.n_tiles], 1);
+            *flag = (old == a.n_tiles - 1);
+          }
+          named_bar(1, kEpiT);
+          const int last = *flag;
+          named_bar(1, kEpiT);
+          if (last) {
+            __threadfence();
+            if (et < a.T) {
+              const volatile float* av = a.arg_val;
+              const volatile int* ai = a.arg_idx;
+              float bv = av[et];
+              int bi = ai[et];
+              for (int tt = 1; tt < a.n_tiles; ++tt) {
+                const float ov = av[(size_t)tt * TMAX + et];
+                const int oi = ai[(size_t)tt * TMAX + et];
+                if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+              }
+              if (a.arg_rec != nullptr)
+                a.arg_rec[et] = make_int2(__float_as_int(bv), bi + a.arg_off);
+              else
+                a.argmax_out[et] = bi;
+            }
+            if (et == 0) a.counters[a.n_tiles] = 0;
+          }
         }
-      }
-      if constexpr (OPC == kOpStore) {
-        if (a.emit == kEmitRms) emit_rms<L, kEpiT, C::kEpiWarps>(a, reinterpret_cast<float*>(smem + C::kStgOff), tile, et);
-      } else if constexpr (OPC == kOpSiluMul) {
-        if (a.emit == kEmitSilu) emit_silu<L, kEpiT, C::kEpiWarps>(a, tile, et, flag);
+        int* const sig = CHAIN && j + 1 < nlin ? ready + j + 1 : nullptr;  // chain: publish the emitted chunk
+        if constexpr (OP == kOpStore) {
+          if (a.emit == kEmitRms)
+            emit_rms<L, TMAX, kEpiT, C::kEpiWarps, CHAIN>(a, reinterpret_cast<float*>(smem + C::kStgOff), tile, et, sig);
+        }
+        if constexpr (OP == kOpSiluMul) {
+          if (a.emit == kEmitSilu) emit_silu<L, TMAX, kEpiT, C::kEpiWarps, CHAIN>(a, tile, et, flag, sig);
+        }
+      };
+      if constexpr (OPC == kOpAny) {
+        switch (a.op) {
+          case kOpSiluMul: post(std::integral_constant<int, kOpSiluMul>{}); break;
+          case kOpQkvRope: post(std::integral_constant<int, kOpQkvRope>{}); break;
+          case kOpLogits: post(std::integral_constant<int, kOpLogits>{}); break;
+          default: post(std::integral_constant<int, kOpStore>{}); break;
+        }
+      } else {
+        post(std::integral_constant<int, OPC>{});
       }
 #pragma unroll
       for (int t = 0; t < kOwn * 8; ++t) acc[t] = 0.f;
     }
+    }
   }
-  if (QS_LIN_TIMELINE && a.dbg && warp == 4 + C::kUnpackWarps && lane == 0) a.dbg[5632 + c] = gtimer();
+#undef QS_LIN_GEOM
+  if (QS_LIN_TIMELINE && A[0].dbg && warp == 4 + C::kUnpackWarps && lane == 0) A[0].dbg[5632 + c] = gtimer();
   tc_fence_before();
   __syncthreads();
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc<C::kTmemCols>(tmem);
   }
-  if (QS_LIN_TIMELINE && a.dbg && threadIdx.x == 0) a.dbg[2048 + c] = gtimer();
-  ktrace_exit(a.kt);
+  if (CHAIN && threadIdx.x == 0) {
+    // every CTA is past its last ready[] read: the last one out re-arms the chain counters
+    if (atomicAdd(exit_cnt, 1) == (int)gridDim.x - 1) {
+      for (int j = 1; j < nlin; ++j) ready[j] = 0;
+      *exit_cnt = 0;
+    }
+  }
+  if (QS_LIN_TIMELINE && A[0].dbg && threadIdx.x == 0) A[0].dbg[2048 + c] = gtimer();
+  ktrace_exit(A[0].kt);
 }
+
+template <int L, int TMAX, int OPC>
+__global__ void __launch_bounds__(LinCfg<L, TMAX>::kThreads, 1) linear_tc_kernel(const __grid_constant__ LinearArgs a) {
+  linear_body<L, TMAX, OPC, false>(&a, 1, nullptr, nullptr);
+}
+
+template <int L, int TMAX>
+__global__ void __launch_bounds__(LinCfg<L, TMAX>::kThreads, 1)
+    linear_chain_kernel(const __grid_constant__ LinearChain ch) {
+  linear_body<L, TMAX, kOpAny, true>(ch.lin, ch.n, ch.ready, ch.exit_cnt);
+}
+
+
 
 template <int L, int TMAX, int OPC>
 static cudaError_t launch_linear_op(const LinearArgs& a, cudaStream_t st) {
@@ -914,6 +1147,44 @@ cudaError_t launch_linear(int L, const LinearArgs& a, cudaStream_t st) {
     case 16: return launch_linear_t<3, 16>(a, st);
     case 32: return launch_linear_t<3, 32>(a, st);
     default: return launch_linear_t<3, 64>(a, st);
+  }
+}
+
+template <int L, int TMAX>
+static cudaError_t launch_chain_t(const LinearChain& ch, cudaStream_t st) {
+  using C = LinCfg<L, TMAX>;
+  static bool attr[kMaxDevices] = {};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev >= kMaxDevices || !attr[dev]) {
+    e = cudaFuncSetAttribute(linear_chain_kernel<L, TMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             C::kSmemBytes);
+    if (e != cudaSuccess) return e;
+    if (dev < kMaxDevices) attr[dev] = true;
+  }
+  for (int j = 0; j < ch.n; ++j)
+    if (ch.lin[j].r_pad != C::kRowsMax || ch.lin[j].n_cta != ch.lin[0].n_cta) return cudaErrorInvalidValue;
+  return launch_k(linear_chain_kernel<L, TMAX>, dim3(ch.lin[0].n_cta), dim3(C::kThreads), C::kSmemBytes, st, ch);
+}
+
+// One launch for a chain of dependent linears (T <= 16 buckets).
+cudaError_t launch_linear_chain(int L, const LinearChain& ch, cudaStream_t st) {
+  if (ch.n < 1 || ch.n > kMaxChain) return cudaErrorInvalidValue;
+  const int tm = linear_tmax_bucket(ch.lin[0].T, L);
+  if (L == 1) {
+    switch (tm) {
+      case 8: return launch_chain_t<1, 8>(ch, st);
+      case 16: return launch_chain_t<1, 16>(ch, st);
+      default: return cudaErrorInvalidValue;
+    }
+  }
+  switch (tm) {
+    case 2: return launch_chain_t<3, 2>(ch, st);
+    case 4: return launch_chain_t<3, 4>(ch, st);
+    case 8: return launch_chain_t<3, 8>(ch, st);
+    case 16: return launch_chain_t<3, 16>(ch, st);
+    default: return cudaErrorInvalidValue;
   }
 }
 

@@ -15,6 +15,7 @@
 
 namespace qs {
 cudaError_t launch_linear(int L, const LinearArgs& a, cudaStream_t st);
+cudaError_t launch_linear_chain(int L, const LinearChain& ch, cudaStream_t st);
 int linear_tmax_bucket(int T, int L);
 cudaError_t launch_act_pack(int L, const PackArgs& a, cudaStream_t st);
 cudaError_t launch_attention(const AttnArgs& a, int n_blk, cudaStream_t st);
@@ -82,6 +83,8 @@ KTrace next_trace(int32_t tag) {
 constexpr int kMaxT = 64;
 constexpr int kGbarOffset = 4096;  // emit counters live past every per-tile counter
 constexpr int kEmitCnt = 8 + 1024;  // [0] arrive, [1] depart, [8 + q] per silu group
+constexpr int kChainOff = kGbarOffset + kEmitCnt + kMaxT * 128;  // chain ready[kMaxChain] + exit counter
+constexpr int kChainCnt = 8;
 
 int g_num_sms = 0;
 
@@ -404,7 +407,8 @@ int qs_workspace_size(const qs_model_t* m, int32_t t_max, qs_workspace_sizes_t* 
   out->ascale = 2 * (size_t)chunks * kMaxT * 4 * 5;  // two slots of ascale + acorr [n_chunks][a_ld][4]
   out->part = (size_t)(num_sms() + tiles) * kMaxT * kTileN * 4;
   // per-tile counters | emit counters [kGbarOffset, +8 + 1024) | emit leaf sums [kMaxT][<=128]
-  out->counters = (size_t)(kGbarOffset + kEmitCnt + kMaxT * 128) * 4;
+  // | chain counters [8]
+  out->counters = (size_t)(kChainOff + kChainCnt) * 4;
   if (tiles + 1 > kGbarOffset) return QS_ERR_SHAPE;
   out->arg_val = (size_t)wl.n_tiles * kMaxT * 4;
   out->arg_idx = (size_t)wl.n_tiles * kMaxT * 4;
@@ -597,9 +601,12 @@ void set_emit(LinearArgs& a, int kind, const qs_qweight_t& next, const Slot& sl,
   a.e_rotate = g_rotate;
   a.e_leaf = reinterpret_cast<float*>(ws->counters + kGbarOffset + kEmitCnt);
 }
-int g_emit = -1;  // fused next-operand emits (mask: 1 silu, 2 rmsnorm): -1 = QS_EMIT env (default 3)
+// fused next-operand emits (mask: 1 silu, 2 rmsnorm, 4 chained launches): -1 = QS_EMIT env,
+// default 3.  Chains (4) are bit-identical but measured slower: PDL already
+// hides the next linear's ramp, and the chained kernel's run-time argument indexing costs more.
+int g_emit = -1;
 int emit_mask() {
-  if (g_emit < 0) g_emit = env_int("QS_EMIT", 3) & 3;
+  if (g_emit < 0) g_emit = env_int("QS_EMIT", 3) & 7;
   return g_emit;
 }
 
@@ -670,7 +677,11 @@ int forward_impl(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const q
   int lin_j = 0;
   const int s0 = 0;            // slot read by qkv / gate_up / lm_head
   bool qkv_ready = false;      // qkv's operand already emitted by the previous down_proj
-  for (int li = 0; li < m->n_layers; ++li) {
+  // Chained launches (LinearChain): with both emits on, o_proj -> gate_up -> down_proj ->
+  // next q|k|v (lm_head after the last layer) run as ONE persistent launch when every
+  // linear of the chain spans the whole grid (units >= #SMs).  Emit mask bit 4.
+  bool chained = false;        // this layer's qkv (or the lm_head) already ran in a chain
+  auto qkv_args = [&](int li) {
     const qs_layer_t& ly = m->layers[li];
     // q|k|v projection; operand = rmsnorm(x) (+ embedding gather on layer 0), fused
     // pre-phase; epilogue: RoPE + KV write (model.py:302-309, 339-340)
@@ -697,8 +708,30 @@ int forward_impl(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const q
     a.block_table = m->block_table;
     a.bt_ld = m->bt_ld;
     a.page = m->page;
-    ws_stream.window(a, lin_j++);
-    if ((e = launch_linear_packed(L, a, st, mode * 16 + 0, !qkv_ready)) != cudaSuccess) return status(e);
+    return a;
+  };
+  const qs_tp_t* tp2 = tp ? tp->tp2 : nullptr;
+  auto head_args = [&]() {
+    // final norm + lm_head + argmax (model.py:342-344, numerics.py:81-86)
+    LinearArgs a = linear_args(m->lm_head, T, L, ws, kOpLogits, logits, m->vocab);
+    a.pk = pack_args(m->lm_head, ws->x, d, T, ws, L);
+    a.pk.rms_w = m->final_norm;
+    a.pk.eps = m->norm_eps;
+    use_slot(a, m->lm_head, slot[s0]);
+    a.argmax_out = argmax;
+    if (tp2) {  // vocab-split head: per-rank (max, index) records, gathered and reduced below
+      a.arg_rec = reinterpret_cast<int2*>(tp2->scratch);
+      a.arg_off = tp2->vocab_off;
+    }
+    return a;
+  };
+  for (int li = 0; li < m->n_layers; ++li) {
+    const qs_layer_t& ly = m->layers[li];
+    if (!chained) {
+      LinearArgs a = qkv_args(li);
+      ws_stream.window(a, lin_j++);
+      if ((e = launch_linear_packed(L, a, st, mode * 16 + 0, !qkv_ready)) != cudaSuccess) return status(e);
+    }
     // attention (model.py:293-330), split-KV partials
     AttnArgs at{};
     at.q = ws->q;
@@ -731,61 +764,94 @@ int forward_impl(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const q
     prof_mark(st, 0, false);
     // o_proj + residual (model.py:332); its operand pack merges the attention chunks;
     // its epilogue emits gate_up's operand rmsnorm(x) * ffn_norm (model.py:333)
-    a = linear_args(ly.o, T, L, ws, res_op, res_out, d);
-    a.pk = pack_args(ly.o, ws->attn, ly.o.k, T, ws, L);
-    a.pk.att_o = ws->att_o;
-    a.pk.att_ml = ws->att_ml;
-    a.pk.att_pos = b->positions;
-    a.pk.att_hd = hd;
-    a.pk.att_cmax = att_cmax;
-    a.pk.att_chunk = attention_chunk_len();
-    use_slot(a, ly.o, slot[s0 ^ 1]);
-    if (emit_rms) set_emit(a, kEmitRms, ly.gate_up, slot[s0], ly.ffn_norm, m->norm_eps, d, ws);
-    ws_stream.window(a, lin_j++);
-    if ((e = launch_linear_packed(L, a, st, mode * 16 + 1)) != cudaSuccess) return status(e);
+    LinearArgs ao = linear_args(ly.o, T, L, ws, res_op, res_out, d);
+    ao.pk = pack_args(ly.o, ws->attn, ly.o.k, T, ws, L);
+    ao.pk.att_o = ws->att_o;
+    ao.pk.att_ml = ws->att_ml;
+    ao.pk.att_pos = b->positions;
+    ao.pk.att_hd = hd;
+    ao.pk.att_cmax = att_cmax;
+    ao.pk.att_chunk = attention_chunk_len();
+    use_slot(ao, ly.o, slot[s0 ^ 1]);
+    if (emit_rms) set_emit(ao, kEmitRms, ly.gate_up, slot[s0], ly.ffn_norm, m->norm_eps, d, ws);
+    ws_stream.window(ao, lin_j++);
+    // gate|up on rmsnorm(x), epilogue silu(gate) * up (model.py:333-335), then down_proj's
+    // operand groups
+    LinearArgs agu = linear_args(ly.gate_up, T, L, ws, kOpSiluMul, ws->h, ff);
+    agu.pk = pack_args(ly.gate_up, ws->x, d, T, ws, L);
+    agu.pk.rms_w = ly.ffn_norm;
+    agu.pk.eps = m->norm_eps;
+    use_slot(agu, ly.gate_up, slot[s0]);
+    if (emit_silu) set_emit(agu, kEmitSilu, ly.down, slot[s0 ^ 1], nullptr, 0.f, ff, ws);
+    ws_stream.window(agu, lin_j++);
+    // down_proj + residual (model.py:336); epilogue emits the next qkv's (or lm_head's)
+    // operand rmsnorm(x) * attn_norm / final_norm (model.py:302, 342)
+    LinearArgs adn = linear_args(ly.down, T, L, ws, res_op, res_out, d);
+    adn.pk = pack_args(ly.down, ws->h, ff, T, ws, L);
+    use_slot(adn, ly.down, slot[s0 ^ 1]);
+    const bool last = li + 1 == m->n_layers;
+    if (emit_rms)
+      set_emit(adn, kEmitRms, last ? m->lm_head : m->layers[li + 1].qkv, slot[s0],
+               last ? m->final_norm : m->layers[li + 1].attn_norm, m->norm_eps, d, ws);
+    ws_stream.window(adn, lin_j++);
+    LinearChain ch{};
+    if ((emit_mask() & 4) && emit_rms && emit_silu) {
+      ch.lin[0] = ao;
+      ch.lin[1] = agu;
+      ch.lin[2] = adn;
+      ch.lin[3] = last ? head_args() : qkv_args(li + 1);
+      ch.n = 4;
+      for (int j = 0; j < ch.n; ++j)
+        if (ch.lin[j].n_cta != num_sms()) ch.n = 0;
+    }
+    if (ch.n > 0) {
+      ws_stream.window(ch.lin[3], lin_j++);
+      ch.ready = ws->counters + kChainOff;
+      ch.exit_cnt = ws->counters + kChainOff + kMaxChain;
+      // o_proj's operand pack (attention merge + quantise), then the chain
+      prof_mark(st, mode * 16 + 5, true);  // kind 5: operand pack
+      ch.lin[0].pk.kt = next_trace(mode * 16 + 5);
+      if ((e = launch_act_pack(L, ch.lin[0].pk, st)) != cudaSuccess) return status(e);
+      prof_mark(st, 0, false);
+      g_launches += 2;
+      static const int split = env_int("QS_CHAIN_SPLIT", 0);  // experiment: one chain launch per linear
+      if (split) {
+        for (int j = 0; j < ch.n; ++j) {
+          LinearChain c1 = ch;
+          c1.lin[0] = ch.lin[j];
+          c1.n = 1;
+          c1.lin[0].kt = next_trace(mode * 16 + 7);
+          prof_mark(st, mode * 16 + 7, true);
+          if ((e = launch_linear_chain(L, c1, st)) != cudaSuccess) return status(e);
+          prof_mark(st, 0, false);
+        }
+        g_launches += ch.n - 1;
+      } else {
+      ch.lin[0].kt = next_trace(mode * 16 + 7);  // kind 7: chained o | gate_up | down | next
+      prof_mark(st, mode * 16 + 7, true);
+      if ((e = launch_linear_chain(L, ch, st)) != cudaSuccess) return status(e);
+      prof_mark(st, 0, false);
+      }
+      chained = true;
+      qkv_ready = true;
+      continue;
+    }
+    chained = false;
+    if ((e = launch_linear_packed(L, ao, st, mode * 16 + 1)) != cudaSuccess) return status(e);
     if (tp) {
       const int rc = reduce_into_x();
       if (rc) return rc;
     }
-    // gate|up on rmsnorm(x), epilogue silu(gate) * up (model.py:333-335), then down_proj's
-    // operand groups
-    a = linear_args(ly.gate_up, T, L, ws, kOpSiluMul, ws->h, ff);
-    a.pk = pack_args(ly.gate_up, ws->x, d, T, ws, L);
-    a.pk.rms_w = ly.ffn_norm;
-    a.pk.eps = m->norm_eps;
-    use_slot(a, ly.gate_up, slot[s0]);
-    if (emit_silu) set_emit(a, kEmitSilu, ly.down, slot[s0 ^ 1], nullptr, 0.f, ff, ws);
-    ws_stream.window(a, lin_j++);
-    if ((e = launch_linear_packed(L, a, st, mode * 16 + 2, !emit_rms)) != cudaSuccess) return status(e);
-    // down_proj + residual (model.py:336); epilogue emits the next qkv's (or lm_head's)
-    // operand rmsnorm(x) * attn_norm / final_norm (model.py:302, 342)
-    a = linear_args(ly.down, T, L, ws, res_op, res_out, d);
-    a.pk = pack_args(ly.down, ws->h, ff, T, ws, L);
-    use_slot(a, ly.down, slot[s0 ^ 1]);
-    const bool last = li + 1 == m->n_layers;
-    if (emit_rms)
-      set_emit(a, kEmitRms, last ? m->lm_head : m->layers[li + 1].qkv, slot[s0],
-               last ? m->final_norm : m->layers[li + 1].attn_norm, m->norm_eps, d, ws);
-    ws_stream.window(a, lin_j++);
-    if ((e = launch_linear_packed(L, a, st, mode * 16 + 3, !emit_silu)) != cudaSuccess) return status(e);
+    if ((e = launch_linear_packed(L, agu, st, mode * 16 + 2, !emit_rms)) != cudaSuccess) return status(e);
+    if ((e = launch_linear_packed(L, adn, st, mode * 16 + 3, !emit_silu)) != cudaSuccess) return status(e);
     if (tp) {
       const int rc = reduce_into_x();
       if (rc) return rc;
     }
     qkv_ready = emit_rms;
   }
-  // final norm + lm_head + argmax (model.py:342-344, numerics.py:81-86)
-  LinearArgs a = linear_args(m->lm_head, T, L, ws, kOpLogits, logits, m->vocab);
-  a.pk = pack_args(m->lm_head, ws->x, d, T, ws, L);
-  a.pk.rms_w = m->final_norm;
-  a.pk.eps = m->norm_eps;
-  use_slot(a, m->lm_head, slot[s0]);
-  a.argmax_out = argmax;
-  const qs_tp_t* tp2 = tp ? tp->tp2 : nullptr;
-  if (tp2) {  // vocab-split head: per-rank (max, index) records, gathered and reduced below
-    a.arg_rec = reinterpret_cast<int2*>(tp2->scratch);
-    a.arg_off = tp2->vocab_off;
-  }
+  if (chained) return QS_OK;  // the lm_head ran in the last chain (never under TP)
+  LinearArgs a = head_args();
   ws_stream.window(a, lin_j++);
   e = launch_linear_packed(L, a, st, mode * 16 + 4, !qkv_ready);
   if (e != cudaSuccess || !tp2) return status(e);
@@ -811,7 +877,7 @@ int qs_forward_tp2(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const
 }
 
 int qs_set_emit(int32_t mask) {
-  g_emit = mask & 3;
+  g_emit = mask & 7;
   return QS_OK;
 }
 

@@ -26,8 +26,8 @@ C8B2 = dict(n_layers=2, d_model=4096, n_heads=32, n_kv_heads=8, d_ff=14336, voca
             rope_theta=500000.0, group_size=128)
 
 
-def _run(model, ids, low, emit):
-    _lib.call("qs_set_emit", 3 if emit else 0)
+def _run(model, ids, low, mask):
+    _lib.call("qs_set_emit", mask)
     try:
         kv = Q.KVCache(model.config)
         logits, arg = run_forward_chunks(model, kv, ids, 0, low)
@@ -45,14 +45,18 @@ def test_emit_bit_identical_to_pack(cfg, T, low):
     kw = {"tiny": TINY, "7b2": C7B2, "8b2": C8B2}[cfg]
     model = Q.random_init(Q.ModelConfig(**kw), 0)
     ids = [int(t) for t in np.random.default_rng(T).integers(0, model.config.vocab_size, T)]
-    l1, a1, k1, n1 = _run(model, ids, low, True)
-    l0, a0, k0, n0 = _run(model, ids, low, False)
-    assert np.array_equal(a1, a0)
-    assert np.array_equal(l1, l0), np.abs(l1 - l0).max()
-    assert all(torch.equal(x, y) for x, y in zip(k1, k0))
+    l0, a0, k0, n0 = _run(model, ids, low, 0)
     L = model.config.n_layers
     assert n0 == 9 * L + 2
-    assert n1 == 6 * L + 2, n1   # qkv, attention, attention-merge pack, o, gate_up, down per layer
+    for mask in (3, 7):
+        l1, a1, k1, n1 = _run(model, ids, low, mask)
+        assert np.array_equal(a1, a0), mask
+        assert np.array_equal(l1, l0), (mask, np.abs(l1 - l0).max())
+        assert all(torch.equal(x, y) for x, y in zip(k1, k0)), mask
+        if mask == 3 or cfg == "tiny":   # tiny: linears narrower than the grid never chain
+            assert n1 == 6 * L + 2, n1   # qkv, attention, attention-merge pack, o, gate_up, down per layer
+        else:   # layer 0: pack, qkv, attention, pack, chain; then attention, pack, chain
+            assert n1 == 3 * L + 2, n1
 
 
 def test_emit_decode_tokens_match_pack_path():
