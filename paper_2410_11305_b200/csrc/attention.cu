@@ -22,10 +22,7 @@ namespace qs {
 #endif
 constexpr int kAttnChunk = QS_ATTN_CHUNK;
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) { cp_async16_cg(smem, gmem); }
 
 // Scores of keys jj = warp + 8u (u < KPW) for every query, QB queries at a time:
 // per (key, query) a lane-ordered fma chain then p += shfl_xor(p, 16..1); the

@@ -54,6 +54,7 @@
 #ifndef QS_U8E8_T
 #define QS_U8E8_T 0
 #endif
+
 // research ablations (scripts/lin_ablate.sh), 0 in the product build; bit 0: unpack skips
 // LDS + ALU, 1: no MMAs (commits only), 2: epilogue skips TMEM loads + math, 3: unpack
 // skips tcgen05.st, 4: no weight bulk copies (the ring fills without HBM traffic)
@@ -257,6 +258,7 @@ __device__ __forceinline__ void emit_rms(const LinearArgs& a, float* stg, int ti
     }
   }
   named_bar(1, kEpiT);
+  if (QS_LIN_TIMELINE && a.dbg && et == 0) a.dbg[7168 + blockIdx.x] = gtimer();  // owner barrier passed
   float* inv = stg + 128 * (a.T > 8 ? a.T : 8);
   const int nl = a.n_tiles, per = nl > 32 ? nl >> 5 : 1, lanes = nl > 32 ? 32 : nl;
   // every leaf load of this warp's tokens in flight at once, then the pairwise sums
@@ -286,13 +288,10 @@ __device__ __forceinline__ void emit_rms(const LinearArgs& a, float* stg, int ti
     }
   }
   named_bar(1, kEpiT);
-  if (et == 0) {  // the last owner through resets both counters (every owner is past the wait)
-    if (atomicAdd(&a.e_cnt[1], 1) == a.n_tiles - 1) {
-      a.e_cnt[0] = 0;
-      a.e_cnt[1] = 0;
-    }
-  }
-#pragma unroll
+  // rolled on purpose: the tail runs once per owner with a cold instruction cache, and
+  // one loop body fetched once beats kTW unrolled copies (measured: down_proj T=16 emit
+  // 4.9 -> 3.0 us from the owner barrier to the quantised chunk)
+#pragma unroll 1
   for (int k = 0; k < kTW; ++k) {
     const int t = ew + k * kEpiWarps;
     if (t >= a.T) break;
@@ -301,6 +300,13 @@ __device__ __forceinline__ void emit_rms(const LinearArgs& a, float* stg, int ti
     const float v[4] = {__fmul_rn(__fmul_rn(xv.x, iv), wv.x), __fmul_rn(__fmul_rn(xv.y, iv), wv.y),
                         __fmul_rn(__fmul_rn(xv.z, iv), wv.z), __fmul_rn(__fmul_rn(xv.w, iv), wv.w)};
     quant_group_warp<L>(v, t, tile, lane, a.e_img, a.e_ascale, a.e_acorr, a.r_pad, a.a_ld, a.e_rotate != 0);
+  }
+  if (QS_LIN_TIMELINE && a.dbg && et == 0) a.dbg[7680 + blockIdx.x] = gtimer();  // quantised
+  if (et == 0) {  // the last owner through resets both counters (every owner is past the wait)
+    if (atomicAdd(&a.e_cnt[1], 1) == a.n_tiles - 1) {
+      a.e_cnt[0] = 0;
+      a.e_cnt[1] = 0;
+    }
   }
   emit_publish<kEpiT, kSignal>(sig, et);
 }
@@ -324,7 +330,7 @@ __device__ __forceinline__ void emit_silu(const LinearArgs& a, int tile, int et,
     hv[k] = t < a.T ? __ldcg(reinterpret_cast<const float4*>(a.out + (size_t)t * a.ldo + 128 * q) + lane)
                     : make_float4(0.f, 0.f, 0.f, 0.f);
   }
-#pragma unroll
+#pragma unroll 1  // (see emit_rms)
   for (int k = 0; k < kTW; ++k) {
     const int t = ew + k * kEpiWarps;
     if (t >= a.T) break;
@@ -852,6 +858,22 @@ __device__ __forceinline__ void linear_body(const LinearArgs* __restrict__ A, co
       if (QS_LIN_TIMELINE && a.dbg && et == 0) a.dbg[3584 + c] = gtimer();
       const int c_lo = cta_of_unit(tile * NC, U, P);
       const int c_hi = cta_of_unit(tile * NC + NC - 1, U, P);
+      // The tail is a chain of dependent global round trips, each ~1-2 us while the next
+      // launch streams its weights: the residual rows (independent of the contributors)
+      // and then every contributor partial go out as 16-byte async copies, one wait each.
+      float* const stg = reinterpret_cast<float*>(smem + C::kStgOff);
+      bool res_staged = false;
+      if constexpr (OPC == kOpStore || OPC == kOpAny) {
+        res_staged = a.op == kOpResidual && (a.n & 3) == 0 && !(c_hi > c_lo && c != c_lo);
+        if (res_staged) {
+          named_bar(1, kEpiT);  // the previous tile's readers of the staging rows are done
+          const int n0 = tile * kTileN;
+          for (int idx = et; idx < a.T * 32; idx += kEpiT) {
+            const int t = idx >> 5, q = idx & 31;
+            if (n0 + 4 * q < a.n) cp_async16_cg(stg + t * 128 + 4 * q, a.out + (size_t)t * a.ldo + n0 + 4 * q);
+          }
+        }
+      }
       if (c_hi > c_lo) {
         // Tile split across CTAs c_lo..c_hi.  Non-owners publish their partial and
         // leave (release-increment, no round trip); the owner c_lo -- whose segment
@@ -883,27 +905,61 @@ __device__ __forceinline__ void linear_body(const LinearArgs* __restrict__ A, co
           if (QS_LIN_TIMELINE && a.dbg) a.dbg[5120 + c] = gtimer();
         }
         named_bar(1, kEpiT);
-        constexpr int kPB = C::kThreads > 512 ? 1 : (kOwn <= 1 ? 4 : (kOwn == 2 ? 2 : 1));
-        for (int cb = c_lo + 1; cb <= c_hi; cb += kPB) {
-          float pv[kPB][kOwn * 8];
+        if constexpr (CHAIN) {
+          // a chain's ring already streams the next linear: partials through registers
+          constexpr int kPB = C::kThreads > 512 ? 1 : (kOwn <= 1 ? 4 : (kOwn == 2 ? 2 : 1));
+          for (int cb = c_lo + 1; cb <= c_hi; cb += kPB) {
+            float pv[kPB][kOwn * 8];
 #pragma unroll
-          for (int u = 0; u < kPB; ++u) {
-            const float* pp = a.part + ((size_t)(cb + u + tile) * TMAX) * kTileN;
+            for (int u = 0; u < kPB; ++u) {
+              const float* pp = a.part + ((size_t)(cb + u + tile) * TMAX) * kTileN;
+#pragma unroll
+              for (int lc = 0; lc < kOwn; ++lc)
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                  const int t = (kH * lc + h) * 8 + e;
+                  pv[u][lc * 8 + e] = (cb + u <= c_hi && t < a.T) ? __ldcg(pp + t * kTileN + r) : 0.f;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kPB; ++u)
+              if (cb + u <= c_hi)
+#pragma unroll
+                for (int k2 = 0; k2 < kOwn * 8; ++k2) acc[k2] = __fadd_rn(acc[k2], pv[u][k2]);
+          }
+        } else {
+        // the owner's segment is its last one: the whole stage ring is drained and free
+        float* const pst = reinterpret_cast<float*>(smem);
+        constexpr int kRing = C::kStages * C::kStageBytes / 4;  // floats
+        static_assert(kRing >= (TMAX < 8 ? 8 : TMAX) * kTileN, "one partial must fit the ring");
+        const int rowsz = a.T * kTileN, np = c_hi - c_lo, maxp = kRing / rowsz;
+        for (int p0 = 0; p0 < np; p0 += maxp) {
+          const int pn = np - p0 < maxp ? np - p0 : maxp;
+          for (int idx = et; idx < pn * a.T * 32; idx += kEpiT) {
+            const int u = idx / (a.T * 32), rem = idx - u * a.T * 32, t = rem >> 5, q = rem & 31;
+            cp_async16_cg(pst + u * rowsz + t * kTileN + 4 * q,
+                          a.part + ((size_t)(c_lo + 1 + p0 + u + tile) * TMAX + t) * kTileN + 4 * q);
+          }
+          cp_async_wait_all();
+          named_bar(1, kEpiT);
+          for (int u = 0; u < pn; ++u) {
 #pragma unroll
             for (int lc = 0; lc < kOwn; ++lc)
 #pragma unroll
               for (int e = 0; e < 8; ++e) {
                 const int t = (kH * lc + h) * 8 + e;
-                pv[u][lc * 8 + e] = (cb + u <= c_hi && t < a.T) ? __ldcg(pp + t * kTileN + r) : 0.f;
+                if (t < a.T) acc[lc * 8 + e] = __fadd_rn(acc[lc * 8 + e], pst[u * rowsz + t * kTileN + r]);
               }
           }
-#pragma unroll
-          for (int u = 0; u < kPB; ++u)
-            if (cb + u <= c_hi)
-#pragma unroll
-              for (int k2 = 0; k2 < kOwn * 8; ++k2) acc[k2] = __fadd_rn(acc[k2], pv[u][k2]);
+          if (p0 + maxp < np) named_bar(1, kEpiT);  // before the next batch overwrites the ring
+        }
         }
       }
+      if (res_staged) {
+        cp_async_wait_all();
+        named_bar(1, kEpiT);
+      }
+      if (QS_LIN_TIMELINE && a.dbg && et == 0) a.dbg[6144 + c] = gtimer();  // partials summed
       // ---------------------------------------------------------- post-ops
       // one specialised tail per post-op class; a chain (OPC = kOpAny) dispatches once per tile
       auto post = [&](auto opc) {
@@ -917,7 +973,8 @@ __device__ __forceinline__ void linear_body(const LinearArgs* __restrict__ A, co
   #pragma unroll
           for (int k = 0; k < kOwn * 8; ++k) {
             const int t = (kH * (k >> 3) + h) * 8 + (k & 7);
-            pre[k] = (res && t < a.T && valid) ? __ldcg(a.out + (size_t)t * a.ldo + n) : 0.f;
+            pre[k] = (res && t < a.T && valid) ? (res_staged ? stg[t * 128 + r] : __ldcg(a.out + (size_t)t * a.ldo + n))
+                                                : 0.f;
           }
         }
   #pragma unroll
@@ -1039,6 +1096,7 @@ __device__ __forceinline__ void linear_body(const LinearArgs* __restrict__ A, co
             if (et == 0) a.counters[a.n_tiles] = 0;
           }
         }
+        if (QS_LIN_TIMELINE && a.dbg && et == 0) a.dbg[6656 + c] = gtimer();  // post-op stores issued
         int* const sig = CHAIN && j + 1 < nlin ? ready + j + 1 : nullptr;  // chain: publish the emitted chunk
         if constexpr (OP == kOpStore) {
           if (a.emit == kEmitRms)
