@@ -92,38 +92,52 @@ __global__ void __launch_bounds__(256) attn_partial_kernel(const AttnArgs a) {
   float* vt = kt + kAttnChunk * hd;           // [chunk][hd]
   float* sc = vt + kAttnChunk * hd;           // [Q][chunk]
   __shared__ int ctx_s[64];
-  __shared__ long long row_s[kAttnChunk];  // element offset of each key row of the chunk
+  __shared__ __align__(8) uint64_t kv_bar[2];  // [0] K rows landed, [1] V rows landed
 
   const int sl = a.slot[tok0];
   const int* bt = a.block_table + (size_t)sl * a.bt_ld;
+  const int warp = tid >> 5, lane = tid & 31, nw = blockDim.x >> 5;
   if (tid < Q) ctx_s[tid] = a.pos[tok0 + tid / hpk] + 1;
-  // page-table walk once per key row (not once per 16-byte copy)
-  for (int jj = tid; jj < nk; jj += blockDim.x) {
-    const int j = j0 + jj;
-    row_s[jj] = (((long long)bt[j / a.page] * a.KV + kvh) * a.page + (j % a.page)) * hd;
+  if (tid == 0) {
+    mbar_init(&kv_bar[0], 1);
+    mbar_init(&kv_bar[1], 1);
+    fence_mbar_init();
   }
   __syncthreads();
-  // async loads: queries, then the chunk's K and V rows (16 B per op)
+  // The chunk's K and V rows are runs of whole page rows, contiguous within a page
+  // ([page][kv_head][row][hd]): warp 0 walks the page table once per page and issues one
+  // bulk copy per (page, K|V) on two barriers, so the scores start as soon as K has
+  // landed while V is still in flight.  The queries go in with 16-byte async copies.
+  if (warp == 0) {
+    const uint32_t bytes = (uint32_t)nk * hd * 4u;
+    if (lane == 0) {
+      mbar_arrive_expect_tx(&kv_bar[0], bytes);
+      mbar_arrive_expect_tx(&kv_bar[1], bytes);
+    }
+    __syncwarp();
+    const int p_first = j0 / a.page, p_last = (j0 + nk - 1) / a.page;
+    for (int pi = p_first + lane; pi <= p_last; pi += 32) {
+      const int r0 = max(j0, pi * a.page), r1 = min(j0 + nk, (pi + 1) * a.page);
+      const size_t off = (((size_t)bt[pi] * a.KV + kvh) * a.page + (r0 - pi * a.page)) * hd;
+      const uint32_t nb = (uint32_t)(r1 - r0) * hd * 4u;
+      bulk_g2s(kt + (r0 - j0) * hd, a.kcache + off, nb, &kv_bar[0]);
+      bulk_g2s(vt + (r0 - j0) * hd, a.vcache + off, nb, &kv_bar[1]);
+    }
+  }
   const int hd4 = hd >> 2;
   for (int e = tid; e < Q * hd4; e += blockDim.x) {
     const int qi = e / hd4, d4 = e - qi * hd4;
     const int i = qi / hpk, h = kvh * hpk + qi % hpk;
     cp_async16(qv + qi * hd + d4 * 4, a.q + (size_t)(tok0 + i) * a.ldq + (size_t)h * hd + d4 * 4);
   }
-  for (int e = tid; e < nk * hd4; e += blockDim.x) {
-    const int jj = e / hd4, d4 = e - jj * hd4;
-    const size_t row = (size_t)row_s[jj] + d4 * 4;
-    cp_async16(kt + jj * hd + d4 * 4, a.kcache + row);
-    cp_async16(vt + jj * hd + d4 * 4, a.vcache + row);
-  }
   cp_async_wait_all();
   __syncthreads();
+  mbar_wait(&kv_bar[0], 0);
 
   // ---- scores: warp per key, lanes split the head dimension, all queries.  Each
   // warp owns keys jj = warp + nw*u; the (key, query) dot products of a 4-query block
   // are independent, so their xor trees are interleaved (same per-pair arithmetic:
   // lane-ordered fma chain, then p += shfl_xor(p, 16..1)).
-  const int warp = tid >> 5, lane = tid & 31, nw = blockDim.x >> 5;
   constexpr int kKPW = kAttnChunk / 8;  // keys per warp at 8 warps
   if (nw == 8) {
     if (Q == 1)
@@ -175,6 +189,7 @@ __global__ void __launch_bounds__(256) attn_partial_kernel(const AttnArgs a) {
   __syncthreads();
 
   // ---- o_c = sum_j p_j v_j  (thread per (query, dim))
+  mbar_wait(&kv_bar[1], 0);
   for (int e = tid; e < Q * hd; e += blockDim.x) {
     const int qi = e / hd, d = e - qi * hd;
     const float* p = sc + qi * kAttnChunk;
