@@ -78,10 +78,12 @@ __global__ void __launch_bounds__(256) attn_partial_kernel(const AttnArgs a) {
   pdl_launch_dependents();
   pdl_wait();
   const int blk = blockIdx.x, kvh = blockIdx.y, ch = blockIdx.z, tid = threadIdx.x;
-  const int ntok = a.blk_ntok[blk];
+  // the prologue is a chain of dependent global round trips: block -> positions + slot
+  // -> page table -> K / V rows; each level's loads are issued together
+  const int ntok = a.blk_ntok[blk], tok0 = a.blk_tok0[blk];
   if (ntok <= 0) return;
-  const int tok0 = a.blk_tok0[blk];
   const int j0 = ch * kAttnChunk;
+  const int sl = a.slot[tok0];
   int cmax = 0;
   for (int i = 0; i < ntok; ++i) cmax = max(cmax, a.pos[tok0 + i] + 1);
   if (j0 >= cmax) return;
@@ -94,7 +96,6 @@ __global__ void __launch_bounds__(256) attn_partial_kernel(const AttnArgs a) {
   __shared__ int ctx_s[64];
   __shared__ __align__(8) uint64_t kv_bar[2];  // [0] K rows landed, [1] V rows landed
 
-  const int sl = a.slot[tok0];
   const int* bt = a.block_table + (size_t)sl * a.bt_ld;
   const int warp = tid >> 5, lane = tid & 31, nw = blockDim.x >> 5;
   if (tid < Q) ctx_s[tid] = a.pos[tok0 + tid / hpk] + 1;
