@@ -288,6 +288,7 @@ __device__ __forceinline__ void emit_rms(const LinearArgs& a, float* stg, int ti
     }
   }
   named_bar(1, kEpiT);
+  if (QS_LIN_TIMELINE && a.dbg && et == 0) a.dbg[7936 + blockIdx.x] = gtimer();  // 1/rms known
   // rolled on purpose: the tail runs once per owner with a cold instruction cache, and
   // one loop body fetched once beats kTW unrolled copies (measured: down_proj T=16 emit
   // 4.9 -> 3.0 us from the owner barrier to the quantised chunk)

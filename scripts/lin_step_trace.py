@@ -39,7 +39,7 @@ _lib.call("qs_debug_timeline", None)
 d = dbg.cpu().numpy().astype(np.int64)
 names = {1024: "entry", 4096: "pdl_wait_ret", 3072: "first_w_data", 4608: "first_act_mma", 3584: "last_seg_fixup",
          5120: "owner_got_parts", 6144: "parts_summed", 6656: "postop_done", 7168: "rms_barrier",
-         7680: "rms_quantised", 5632: "epi_done", 2048: "exit"}
+         7936: "rms_inv", 7680: "rms_quantised", 5632: "epi_done", 2048: "exit"}
 ent = d[1024:1024 + 148]
 t0 = ent[ent > 0].min()
 print(f"{a.which} layer {a.layer} T={a.batch} mode={a.mode}")
