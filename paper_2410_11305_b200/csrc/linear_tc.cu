@@ -133,9 +133,14 @@ struct LinCfg {
   static constexpr int kOwnChunks = ((TMAX < 8 ? 8 : TMAX) / 8 + kEpiHalves - 1) / kEpiHalves;  // per epilogue warp
   static constexpr int kScaleOff = kStages * kStageBytes;
   static constexpr int kBarOff = kScaleOff + kSStages * kSEntry;
-  static constexpr int kNumBars = 3 * kStages + 2 * kASlots + 2 * kAccBufs + 2 * kSStages;
+  static constexpr int kNumBars = 3 * kStages + 2 * kASlots + 2 * kAccBufs + 2 * kSStages + 1;
   static constexpr int kStgOff = ((kBarOff + kNumBars * 8 + 16 + 4 * TMAX * 8 + 4 * 4 + 32 * 4) + 15) / 16 * 16;
-  static constexpr int kSmemBytes = kStgOff + kStgBytes + 1024;
+  // the rest of the 227 KB: contributor partials of the owned last tile, bulk-copied in by
+  // warp 2 while the owner still streams its own stages
+  static constexpr int kPartOff = (kStgOff + kStgBytes + 127) / 128 * 128;
+  static constexpr int kPartBytes0 = 227 * 1024 - 1024 - kPartOff;
+  static constexpr int kPartBytes = kPartBytes0 > 0 ? kPartBytes0 / 512 * 512 : 0;
+  static constexpr int kSmemBytes = kPartOff + kPartBytes + 1024;
   static_assert(kSmemBytes <= 227 * 1024, "shared memory budget");
 };
 
@@ -366,6 +371,7 @@ __device__ __forceinline__ void linear_body(const LinearArgs* __restrict__ A, co
   uint64_t* accempty = accfull + C::kAccBufs;  // [kAccBufs] epilogue -> MMA
   uint64_t* sfull = accempty + C::kAccBufs;    // [kSStages] scales landed
   uint64_t* sempty = sfull + C::kSStages;      // [kSStages] epilogue -> scale producer
+  uint64_t* pbar = sempty + C::kSStages;       // [1] prefetched contributor partials landed
   float* sring = reinterpret_cast<float*>(smem + C::kScaleOff);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::kNumBars);
   int* flag = reinterpret_cast<int*>(tmem_slot + 2);
@@ -394,6 +400,7 @@ __device__ __forceinline__ void linear_body(const LinearArgs* __restrict__ A, co
       mbar_init(&accempty[i], C::kEpiWarps);
     }
     for (int i = 0; i < C::kSStages; ++i) { mbar_init(&sfull[i], 1); mbar_init(&sempty[i], C::kEpiWarps); }
+    mbar_init(pbar, 1);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc<C::kTmemCols>(tmem_slot);
@@ -608,6 +615,34 @@ __device__ __forceinline__ void linear_body(const LinearArgs* __restrict__ A, co
         mbar_arrive_expect_tx_elect(&sfull[ss], (uint32_t)it.nq * e_bytes);
         bulk_g2s_elect(se, a.wscale + ((size_t)it.tile * NC + it.ch0) * kTileN, it.nq * 512u, &sfull[ss]);
         act_part(se, it, ss);
+      }
+    }
+  } else if (!CHAIN && warp == 2) {
+    // ------------------------------------------------------------ partial prefetch
+    // The owner of a split tile processes that tile's first chunks as its LAST segment;
+    // the contributors processed the rest as their FIRST segments and published long
+    // before.  Warp 2 (idle after the TMEM allocation) waits for them and bulk-copies
+    // their partials into shared memory while the owner still streams, so the owner's
+    // fixup is one mbarrier wait instead of a counter poll plus a gather round trip.
+    QS_LIN_GEOM(0)
+    if (u1 > u0 && !op_is<OPC, kOpDump>(a)) {  // dumps keep per-CTA partials, no fixup
+      const int lt = (u1 - 1) / NC;
+      const int lo = cta_of_unit(lt * NC, U, P), hi = cta_of_unit(lt * NC + NC - 1, U, P);
+      const int np = hi - lo;
+      if (lo == c && np > 0 && np * a.T * kTileN * 4 <= C::kPartBytes && lane == 0) {
+        pdl_wait();  // counters and partial slots are reused across launches
+        const unsigned long long t0 = gtimer();
+        while (ld_acquire(&a.counters[lt]) != np) {
+          if (gtimer() - t0 > 5000000000ull) __trap();
+          __nanosleep(64);
+        }
+        a.counters[lt] = 0;
+        fence_proxy_async_global();  // acquired generic writes -> async-proxy reads
+        const uint32_t rb = (uint32_t)a.T * kTileN * 4u;
+        mbar_arrive_expect_tx(pbar, (uint32_t)np * rb);
+        float* dst = reinterpret_cast<float*>(smem + C::kPartOff);
+        for (int u = 0; u < np; ++u)
+          bulk_g2s(dst + (size_t)u * a.T * kTileN, a.part + ((size_t)(lo + 1 + u + lt) * TMAX) * kTileN, rb, pbar);
       }
     }
   } else if (warp == 1) {
@@ -895,6 +930,22 @@ __device__ __forceinline__ void linear_body(const LinearArgs* __restrict__ A, co
           for (int t = 0; t < kOwn * 8; ++t) acc[t] = 0.f;
           continue;
         }
+        const bool prefetched = !CHAIN && (c_hi - c_lo) * a.T * kTileN * 4 <= C::kPartBytes;
+        if (prefetched) {
+          // warp 2 gathered them (the owner's split tile is always its last segment)
+          mbar_wait_warp(pbar, 0, 0);
+          if (QS_LIN_TIMELINE && a.dbg && et == 0) a.dbg[5120 + c] = gtimer();
+          const float* pp = reinterpret_cast<const float*>(smem + C::kPartOff);
+          for (int u = 0; u < c_hi - c_lo; ++u) {
+#pragma unroll
+            for (int lc = 0; lc < kOwn; ++lc)
+#pragma unroll
+              for (int e = 0; e < 8; ++e) {
+                const int t = (kH * lc + h) * 8 + e;
+                if (t < a.T) acc[lc * 8 + e] = __fadd_rn(acc[lc * 8 + e], pp[(u * a.T + t) * kTileN + r]);
+              }
+          }
+        } else {
         if (et == 0) {
           // same 5 s trap guard as the mbarrier waits: a missing contributor (CTAs not
           // co-resident) fails the launch instead of wedging the GPU
@@ -953,6 +1004,7 @@ __device__ __forceinline__ void linear_body(const LinearArgs* __restrict__ A, co
               }
           }
           if (p0 + maxp < np) named_bar(1, kEpiT);  // before the next batch overwrites the ring
+        }
         }
         }
       }

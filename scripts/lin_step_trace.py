@@ -52,3 +52,16 @@ for off, nm in sorted(names.items(), key=lambda kv: np.median(d[kv[0]:kv[0] + 14
         continue
     p = np.percentile(v, [0, 10, 50, 90, 100]).astype(int)
     print(f"  {nm:16s} n={len(v):3d}  min {p[0]:6d}  p10 {p[1]:6d}  med {p[2]:6d}  p90 {p[3]:6d}  max {p[4]:6d}")
+# per-owner step durations (owners = CTAs that waited for contributor partials)
+own = np.nonzero(d[5120:5120 + 148] > 0)[0]
+if len(own):
+    steps = [(3584, 5120, "own seg end -> partials ready"), (5120, 6144, "partials summed"),
+             (6144, 6656, "post-op"), (6656, 7168, "leaves + owner barrier"), (7168, 7936, "1/rms"),
+             (7936, 7680, "quantise"), (7680, 2048, "-> exit")]
+    print(f"  owners n={len(own)} (median / max ns per step)")
+    for s0, s1, nm in steps:
+        x, y = d[s0 + own], d[s1 + own]
+        ok = (x > 0) & (y > 0)
+        if ok.any():
+            dd = (y - x)[ok]
+            print(f"    {nm:28s} {int(np.median(dd)):6d} {int(dd.max()):6d}")
