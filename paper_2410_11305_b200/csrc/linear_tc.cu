@@ -54,6 +54,12 @@
 #ifndef QS_U8E8_T
 #define QS_U8E8_T 0
 #endif
+// warp-2 contributor-partial prefetch for buckets T <= this (others: the owner polls and
+// gathers).  Measured: B=1 AR 2.36 -> 2.34 ms, B=1 QSpec cycle 10.1 -> 9.9 ms; at T = 16 it
+// cost ~1 % (B=16 16.74 -> 16.91 ms per cycle), so the T = 16 bucket keeps the gather.
+#ifndef QS_PART_PREFETCH_TMAX
+#define QS_PART_PREFETCH_TMAX 8
+#endif
 
 // research ablations (scripts/lin_ablate.sh), 0 in the product build; bit 0: unpack skips
 // LDS + ALU, 1: no MMAs (commits only), 2: epilogue skips TMEM loads + math, 3: unpack
@@ -133,12 +139,13 @@ struct LinCfg {
   static constexpr int kOwnChunks = ((TMAX < 8 ? 8 : TMAX) / 8 + kEpiHalves - 1) / kEpiHalves;  // per epilogue warp
   static constexpr int kScaleOff = kStages * kStageBytes;
   static constexpr int kBarOff = kScaleOff + kSStages * kSEntry;
-  static constexpr int kNumBars = 3 * kStages + 2 * kASlots + 2 * kAccBufs + 2 * kSStages + 1;
+  static constexpr bool kPref = TMAX <= QS_PART_PREFETCH_TMAX;  // warp-2 partial prefetch compiled in
+  static constexpr int kNumBars = 3 * kStages + 2 * kASlots + 2 * kAccBufs + 2 * kSStages + (kPref ? 1 : 0);
   static constexpr int kStgOff = ((kBarOff + kNumBars * 8 + 16 + 4 * TMAX * 8 + 4 * 4 + 32 * 4) + 15) / 16 * 16;
   // the rest of the 227 KB: contributor partials of the owned last tile, bulk-copied in by
   // warp 2 while the owner still streams its own stages
-  static constexpr int kPartOff = (kStgOff + kStgBytes + 127) / 128 * 128;
-  static constexpr int kPartBytes0 = 227 * 1024 - 1024 - kPartOff;
+  static constexpr int kPartOff = kPref ? (kStgOff + kStgBytes + 127) / 128 * 128 : kStgOff + kStgBytes;
+  static constexpr int kPartBytes0 = kPref ? 227 * 1024 - 1024 - kPartOff : 0;
   static constexpr int kPartBytes = kPartBytes0 > 0 ? kPartBytes0 / 512 * 512 : 0;
   static constexpr int kSmemBytes = kPartOff + kPartBytes + 1024;
   static_assert(kSmemBytes <= 227 * 1024, "shared memory budget");
@@ -400,7 +407,7 @@ __device__ __forceinline__ void linear_body(const LinearArgs* __restrict__ A, co
       mbar_init(&accempty[i], C::kEpiWarps);
     }
     for (int i = 0; i < C::kSStages; ++i) { mbar_init(&sfull[i], 1); mbar_init(&sempty[i], C::kEpiWarps); }
-    mbar_init(pbar, 1);
+    if (C::kPref) mbar_init(pbar, 1);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc<C::kTmemCols>(tmem_slot);
@@ -617,7 +624,7 @@ __device__ __forceinline__ void linear_body(const LinearArgs* __restrict__ A, co
         act_part(se, it, ss);
       }
     }
-  } else if (!CHAIN && warp == 2) {
+  } else if (!CHAIN && C::kPref && warp == 2) {
     // ------------------------------------------------------------ partial prefetch
     // The owner of a split tile processes that tile's first chunks as its LAST segment;
     // the contributors processed the rest as their FIRST segments and published long
@@ -930,7 +937,7 @@ __device__ __forceinline__ void linear_body(const LinearArgs* __restrict__ A, co
           for (int t = 0; t < kOwn * 8; ++t) acc[t] = 0.f;
           continue;
         }
-        const bool prefetched = !CHAIN && (c_hi - c_lo) * a.T * kTileN * 4 <= C::kPartBytes;
+        const bool prefetched = !CHAIN && C::kPref && (c_hi - c_lo) * a.T * kTileN * 4 <= C::kPartBytes;
         if (prefetched) {
           // warp 2 gathered them (the owner's split tile is always its last segment)
           mbar_wait_warp(pbar, 0, 0);
