@@ -250,7 +250,7 @@ def critical_path(kt) -> dict:
     bracketed per-launch durations above serialise the graph; this is where the step's time
     actually goes."""
     tags, st, en = kt
-    names = ["qkv", "o", "gate_up", "down", "lm_head", "pack", "attention", "chain"]
+    names = ["qkv", "o", "gate_up", "down", "lm_head", "pack", "attention"]
     per, prev, span = {}, 0.0, float(en.max()) if len(en) else 0.0
     for i in range(len(tags)):
         mode, kind = tags[i] // 16, tags[i] % 16
@@ -260,7 +260,7 @@ def critical_path(kt) -> dict:
         d = per.setdefault(key, [0, 0.0])
         d[0] += 1
         d[1] += exp
-    lin = sum(v[1] for k, v in per.items() if k.split(".")[1] in names[:5] + ["chain"])
+    lin = sum(v[1] for k, v in per.items() if k.split(".")[1] in names[:5])
     return {"span_us": round(span, 1), "linear_exposed_us": round(lin, 1),
             "linear_share": round(lin / span, 3) if span else None,
             "per_kind_exposed_us": {k: round(v[1], 1) for k, v in sorted(per.items(), key=lambda kv: -kv[1][1])},
@@ -274,19 +274,15 @@ def linear_roofline(model, a, prof: list, batch: int, ctx_mean: float) -> dict:
     replayed step, tag = mode*16 + kind, mode 1 = W4A4 draft, 0 = W4A16 verify).
 
     The dominant kernel is linear_tc_kernel; bytes per launch = N*K/2 codes + 4*N*K/g
-    scales + 4*T*K activations + 4*T*N outputs.  A chained launch (kind 7,
-    linear_chain_kernel) carries o_proj, gate_up, down_proj and the next q|k|v -- the
-    lm_head in a forward's last chain -- so its bytes are the sum of those four.
+    scales + 4*T*K activations + 4*T*N outputs.
     """
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     peak = peaks["hbm_gbs"]
     lw = model.layers[0]
     stores = [lw.qkv, lw.o, lw.gate_up, lw.down, model.lm_head.store]
-    names = ["qkv", "o", "gate_up", "down", "lm_head", "pack", "attention", "chain"]
+    names = ["qkv", "o", "gate_up", "down", "lm_head", "pack", "attention", "forward"]
     kinds, other = {}, {}
     tot_b = tot_ms = step_ms = 0.0
-    n_layers = model.config.n_layers
-    chains_seen = {}
 
     def lin_bytes(kind, T):
         st = stores[kind]
@@ -301,9 +297,6 @@ def linear_roofline(model, a, prof: list, batch: int, ctx_mean: float) -> dict:
         key = ("draft" if draft else "verify") + "." + names[kind]
         if kind < 5:
             byts = lin_bytes(kind, T)
-        elif kind == 7:
-            c = chains_seen[mode] = chains_seen.get(mode, 0) + 1
-            byts = sum(lin_bytes(k, T) for k in (1, 2, 3)) + lin_bytes(4 if c % n_layers == 0 else 0, T)
         else:
             d = other.setdefault(key, [0, 0.0])
             d[0] += 1
@@ -320,7 +313,7 @@ def linear_roofline(model, a, prof: list, batch: int, ctx_mean: float) -> dict:
                "GBps": round(v[2] / (v[1] / 1e3) / 1e9, 1)} for k, v in kinds.items()}
     per.update({k: {"launches": v[0], "avg_us": round(1e3 * v[1] / v[0], 2)} for k, v in other.items()})
     n = sum(v[0] for v in kinds.values())
-    kernel = "linear_tc_kernel / linear_chain_kernel (tcgen05 kind::i8), all launches of one replayed step"
+    kernel = "linear_tc_kernel (tcgen05 kind::i8), all launches of one replayed step"
     # DRAM traffic of one captured launch of the dominant kernel (committed ncu summary)
     traffic, traffic_note = None, None
     tf = os.path.join(ROOT, "profiles", "traffic.json")

@@ -221,8 +221,7 @@ int qs_forward_tp2(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const
 int qs_forward_launches(void);
 /* fused next-operand emits, mask: 1 = gate_up's epilogue emits down_proj's operand, 2 = the
    residual epilogues (o_proj, down_proj) emit the RMSNorm'd operand of the next linear;
-   0 = a separate act_pack before every linear; 4 (with 3) = o_proj -> gate_up -> down_proj ->
-   next q|k|v / lm_head as ONE chained launch (opt-in).  Default: QS_EMIT env, else 3. */
+   0 = a separate act_pack before every linear.  Default: QS_EMIT env, else 3. */
 int qs_set_emit(int32_t mask);
 
 int qs_forward_tp(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const qs_workspace_t* ws, float* logits,

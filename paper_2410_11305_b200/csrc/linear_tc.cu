@@ -215,7 +215,6 @@ struct StageIt {
 // covers store / residual / dump (runtime a.op), every other class is exact.
 template <int OPC, int O>
 __device__ __forceinline__ bool op_is(const LinearArgs& a) {
-  if constexpr (OPC == kOpAny) return O != kOpDump && a.op == O;  // chains: never a dump
   constexpr bool in_class = OPC == kOpStore ? (O == kOpStore || O == kOpResidual || O == kOpDump) : O == OPC;
   if constexpr (!in_class) return false;
   if constexpr (OPC != kOpStore) return true;
@@ -228,18 +227,8 @@ __device__ __forceinline__ bool op_is(const LinearArgs& a) {
 // splits down to 128-element leaves, each summed with 8 strided accumulators and the
 // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) bracket; leaves combine as a balanced tree
 // (token_inv_rms in pack_dev.cuh states the same order).
-// Chain launches (kSignal): after quantising, publish the chunk on *sig (release) for the
-// next linear's operand wait.
-template <int kEpiT, bool kSignal>
-__device__ __forceinline__ void emit_publish(int* sig, int et) {
-  if constexpr (kSignal) {
-    if (sig == nullptr) return;
-    named_bar(1, kEpiT);  // the CTA's chunk writes, then one cumulative gpu-scope release
-    if (et == 0) red_release_add(sig, 1);
-  }
-}
-template <int L, int TMAX, int kEpiT, int kEpiWarps, bool kSignal>
-__device__ __forceinline__ void emit_rms(const LinearArgs& a, float* stg, int tile, int et, int* sig) {
+template <int L, int TMAX, int kEpiT, int kEpiWarps>
+__device__ __forceinline__ void emit_rms(const LinearArgs& a, float* stg, int tile, int et) {
   const int lane = et & 31, ew = et >> 5;
   constexpr int kTW = (TMAX + kEpiWarps - 1) / kEpiWarps;  // tokens per warp
   // this tile's RMSNorm weights do not depend on the barrier: in flight across it
@@ -321,13 +310,12 @@ __device__ __forceinline__ void emit_rms(const LinearArgs& a, float* stg, int ti
       a.e_cnt[1] = 0;
     }
   }
-  emit_publish<kEpiT, kSignal>(sig, et);
 }
 
 // kEmitSilu (gate_up): tiles 2q, 2q+1 hold silu outputs 128q..128q+127 = group q of
 // down_proj's input.  Each owner publishes its half; the second one quantises the group.
-template <int L, int TMAX, int kEpiT, int kEpiWarps, bool kSignal>
-__device__ __forceinline__ void emit_silu(const LinearArgs& a, int tile, int et, int* flag, int* sig) {
+template <int L, int TMAX, int kEpiT, int kEpiWarps>
+__device__ __forceinline__ void emit_silu(const LinearArgs& a, int tile, int et, int* flag) {
   constexpr int kTW = (TMAX + kEpiWarps - 1) / kEpiWarps;  // tokens per warp
   const int lane = et & 31, ew = et >> 5, q = tile >> 1;
   named_bar(1, kEpiT);  // the CTA's h writes, then et 0's acq_rel add (cumulative release)
@@ -351,19 +339,11 @@ __device__ __forceinline__ void emit_silu(const LinearArgs& a, int tile, int et,
     quant_group_warp<L>(v, t, q, lane, a.e_img, a.e_ascale, a.e_acorr, a.r_pad, a.a_ld, a.e_rotate != 0);
   }
   if (et == 0) a.e_cnt[8 + q] = 0;
-  emit_publish<kEpiT, kSignal>(sig, et);
 }
 
-// The linear kernel body.  A single launch runs one linear (A = its argument block,
-// nlin = 1); a chain launch (CHAIN, OPC = kOpAny) runs the nlin linears of a
-// LinearChain back to back in one persistent grid: every role walks the chain's
-// linears in order with its ring positions carried across them, so linear j+1's weight
-// stream starts as soon as the ring has room while linear j's fixups and operand emit
-// are still running.  Only linear j+1's activation copies (warp 2 images, warp 3
-// scales) and its epilogue wait for ready[j+1] (every operand chunk emitted).
-template <int L, int TMAX, int OPC, bool CHAIN>
-__device__ __forceinline__ void linear_body(const LinearArgs* __restrict__ A, const int nlin, int* ready,
-                                            int* exit_cnt) {
+// The linear kernel body (A = the launch's argument block).
+template <int L, int TMAX, int OPC>
+__device__ __forceinline__ void linear_body(const LinearArgs* __restrict__ A) {
   using C = LinCfg<L, TMAX>;
   constexpr int CPS = C::kCPS;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -415,8 +395,7 @@ __device__ __forceinline__ void linear_body(const LinearArgs* __restrict__ A, co
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  // per-linear geometry (the chain's linears share T, L and so r_pad; every CTA of a
-  // chain launch holds units of every linear: host checks n_cta == grid)
+  // the launch's unit partition
 #define QS_LIN_GEOM(j)                                   \
   const LinearArgs& a = A[j];                            \
   const int NC = a.n_chunks;                             \
@@ -424,99 +403,7 @@ __device__ __forceinline__ void linear_body(const LinearArgs* __restrict__ A, co
   const int u0 = unit_bound(c, U, P), u1 = unit_bound(c + 1, U, P); \
   (void)u0;                                              \
   (void)u1;
-  // spin (all lanes) until linear j's operand is complete, then order the async-proxy
-  // (bulk copy) reads after the generic-proxy writes of the emitting CTAs
-  auto wait_operand = [&](int j) {
-    const unsigned long long t0 = gtimer();
-    while (ld_acquire(ready + j) < A[j].n_chunks) {
-      if (gtimer() - t0 > 5000000000ull) __trap();
-    }
-    fence_proxy_async_global();
-  };
-  (void)wait_operand;
-
-  if (CHAIN && warp == 0) {
-    // ------------------------------------------------------------ weight producer (chain)
-    int i = 0;  // ring position, carried across the chain's linears
-    for (int j = 0; j < nlin; ++j) {
-      QS_LIN_GEOM(j)
-      if (lane == 0 && a.pf_n > 0) {  // this CTA's share of the look-ahead window
-        size_t tot = 0;
-        for (int r = 0; r < a.pf_n; ++r) tot += a.pf_len[r];
-        size_t lo = (tot * (size_t)c / P) & ~(size_t)15, hi = (tot * (size_t)(c + 1) / P) & ~(size_t)15;
-        if (c == P - 1) hi = tot;
-        size_t base = 0;
-        for (int r = 0; r < a.pf_n && lo < hi; ++r) {
-          const size_t e = base + a.pf_len[r];
-          if (lo < e) {
-            const size_t x0 = lo - base, x1 = (hi < e ? hi : e) - base;
-            for (size_t o = x0; o < x1; o += kPfPiece)
-              prefetch_l2(a.pf_ptr[r] + o, (uint32_t)(x1 - o < kPfPiece ? x1 - o : kPfPiece));
-            lo = base + x1;
-          }
-          base = e;
-        }
-      }
-      __syncwarp();
-      StageIt it{u0, u1, NC, CPS};
-      for (; it.next(); ++i) {
-        const int s = i % C::kStages;
-        mbar_wait(&empty[s], ((i / C::kStages) & 1) ^ 1);  // fresh slots: parity 1 passes
-        mbar_arrive_expect_tx_elect(&wfull[s], (uint32_t)it.nq * kChunkBytes);
-        bulk_g2s_elect(smem + s * C::kStageBytes, a.codes + ((size_t)it.tile * NC + it.ch0) * kChunkBytes,
-                       it.nq * kChunkBytes, &wfull[s]);
-      }
-    }
-  } else if (CHAIN && warp == 2) {
-    // ------------------------------------------------------------ activation-image producer (chain)
-    pdl_wait();
-    int i = 0;
-    for (int j = 0; j < nlin; ++j) {
-      QS_LIN_GEOM(j)
-      const uint32_t act_bytes = (uint32_t)a.r_pad * 128u;
-      if (j > 0) wait_operand(j);
-      StageIt it{u0, u1, NC, CPS};
-      for (; it.next(); ++i) {
-        const int s = i % C::kStages;
-        mbar_wait(&empty[s], ((i / C::kStages) & 1) ^ 1);
-        mbar_arrive_expect_tx_elect(&afull[s], (uint32_t)it.nq * act_bytes);
-        bulk_g2s_elect(smem + s * C::kStageBytes + CPS * kChunkBytes, a.act + (size_t)it.ch0 * act_bytes,
-                       it.nq * act_bytes, &afull[s]);
-      }
-    }
-  } else if (CHAIN && warp == 3) {
-    // ------------------------------------------------------------ scale producer (chain)
-    // weight scales of up to kSStages entries go out before the operand wait, the
-    // activation scales / correction sums of those entries after it
-    int i = 0;
-    for (int j = 0; j < nlin; ++j) {
-      QS_LIN_GEOM(j)
-      const uint32_t a_bytes = (uint32_t)a.a_ld * 4u;
-      const uint32_t e_bytes = 512u + (C::kUns ? 5u : 1u) * a_bytes;
-      auto act_part = [&](const StageIt& st, int ss) {
-        float* se = sring + ss * (C::kSEntry / 4);
-        bulk_g2s_elect(se + CPS * 128, a.ascale + (size_t)st.ch0 * a.a_ld, st.nq * a_bytes, &sfull[ss]);
-        if (C::kUns)
-          bulk_g2s_elect(se + C::kCorrOff, a.acorr + (size_t)st.ch0 * a.a_ld * 4, st.nq * 4u * a_bytes, &sfull[ss]);
-      };
-      auto w_part = [&](const StageIt& st, int ss) {
-        mbar_wait(&sempty[ss], ((i / C::kSStages) & 1) ^ 1);
-        mbar_arrive_expect_tx_elect(&sfull[ss], (uint32_t)st.nq * e_bytes);
-        bulk_g2s_elect(sring + ss * (C::kSEntry / 4), a.wscale + ((size_t)st.tile * NC + st.ch0) * kTileN,
-                       st.nq * 512u, &sfull[ss]);
-      };
-      StageIt it{u0, u1, NC, CPS}, ia{u0, u1, NC, CPS};
-      const int i0 = i;
-      int npro = 0;
-      for (; npro < C::kSStages && it.next(); ++npro, ++i) w_part(it, i % C::kSStages);
-      if (j == 0) pdl_wait(); else wait_operand(j);
-      for (int k = 0; k < npro && ia.next(); ++k) act_part(ia, (i0 + k) % C::kSStages);
-      for (; it.next(); ++i) {
-        w_part(it, i % C::kSStages);
-        act_part(it, i % C::kSStages);
-      }
-    }
-  } else if (!CHAIN && warp == 0) {
+  if (warp == 0) {
     // ------------------------------------------------------------ weight/act producer (warp-wide, elected issue)
     // Weights do not depend on the previous kernel: the first kStages stages of
     // weights are requested before griddepcontrol.wait (PDL overlap); activation
@@ -591,7 +478,7 @@ __device__ __forceinline__ void linear_body(const LinearArgs* __restrict__ A, co
         if (dbg0 && i < 64 && lane == 0) a.dbg[0 * 64 + i] = gtimer();
       }
     }
-  } else if (!CHAIN && warp == 3) {
+  } else if (warp == 3) {
     // ------------------------------------------------------------ scale producer (warp-wide, elected issue)
     // Weight scales do not depend on the previous kernel: the first kSStages entries'
     // weight scales are requested before griddepcontrol.wait (with the whole entry's
@@ -624,7 +511,7 @@ __device__ __forceinline__ void linear_body(const LinearArgs* __restrict__ A, co
         act_part(se, it, ss);
       }
     }
-  } else if (!CHAIN && C::kPref && warp == 2) {
+  } else if (C::kPref && warp == 2) {
     // ------------------------------------------------------------ partial prefetch
     // The owner of a split tile processes that tile's first chunks as its LAST segment;
     // the contributors processed the rest as their FIRST segments and published long
@@ -655,8 +542,8 @@ __device__ __forceinline__ void linear_body(const LinearArgs* __restrict__ A, co
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer (warp-wide, elected issue)
     int i = 0;
-    for (int j = 0; j < nlin; ++j) {
-      QS_LIN_GEOM(j)
+    {
+      QS_LIN_GEOM(0)
       const uint32_t idesc = idesc_i8(128, (uint32_t)a.r_pad, !C::kUns);
       StageIt it{u0, u1, NC, CPS};
       for (; it.next(); ++i) {
@@ -695,8 +582,8 @@ __device__ __forceinline__ void linear_body(const LinearArgs* __restrict__ A, co
     const int q4 = warp & 3, ug = (warp - 4) >> 2, r = q4 * 32 + lane;
     const uint32_t lane_base = (uint32_t)(q4 * 32) << 16;
     int i = 0;
-    for (int j = 0; j < nlin; ++j) {
-    QS_LIN_GEOM(j)
+    {
+    QS_LIN_GEOM(0)
     StageIt it{u0, u1, NC, CPS};
     for (; it.next(); ++i) {
       if ((i % C::kUnpackHalves) != ug) continue;
@@ -769,17 +656,8 @@ __device__ __forceinline__ void linear_body(const LinearArgs* __restrict__ A, co
 #pragma unroll
     for (int t = 0; t < kOwn * 8; ++t) acc[t] = 0.f;
     int i = 0;
-    for (int j = 0; j < nlin; ++j) {
-    QS_LIN_GEOM(j)
-    if (CHAIN && j > 0) {  // the residual rows / h this linear reads were written by earlier ones
-      if (et == 0) {
-        const unsigned long long t0 = gtimer();
-        while (ld_acquire(ready + j) < a.n_chunks) {
-          if (gtimer() - t0 > 5000000000ull) __trap();
-        }
-      }
-      named_bar(1, kEpiT);
-    }
+    {
+    QS_LIN_GEOM(0)
     StageIt it{u0, u1, NC, CPS};
     for (; it.next(); ++i) {
       const int b = i % C::kAccBufs, ss = i % C::kSStages;
@@ -906,7 +784,7 @@ __device__ __forceinline__ void linear_body(const LinearArgs* __restrict__ A, co
       // and then every contributor partial go out as 16-byte async copies, one wait each.
       float* const stg = reinterpret_cast<float*>(smem + C::kStgOff);
       bool res_staged = false;
-      if constexpr (OPC == kOpStore || OPC == kOpAny) {
+      if constexpr (OPC == kOpStore) {
         res_staged = a.op == kOpResidual && (a.n & 3) == 0 && !(c_hi > c_lo && c != c_lo);
         if (res_staged) {
           named_bar(1, kEpiT);  // the previous tile's readers of the staging rows are done
@@ -937,7 +815,7 @@ __device__ __forceinline__ void linear_body(const LinearArgs* __restrict__ A, co
           for (int t = 0; t < kOwn * 8; ++t) acc[t] = 0.f;
           continue;
         }
-        const bool prefetched = !CHAIN && C::kPref && (c_hi - c_lo) * a.T * kTileN * 4 <= C::kPartBytes;
+        const bool prefetched = C::kPref && (c_hi - c_lo) * a.T * kTileN * 4 <= C::kPartBytes;
         if (prefetched) {
           // warp 2 gathered them (the owner's split tile is always its last segment)
           mbar_wait_warp(pbar, 0, 0);
@@ -964,29 +842,6 @@ __device__ __forceinline__ void linear_body(const LinearArgs* __restrict__ A, co
           if (QS_LIN_TIMELINE && a.dbg) a.dbg[5120 + c] = gtimer();
         }
         named_bar(1, kEpiT);
-        if constexpr (CHAIN) {
-          // a chain's ring already streams the next linear: partials through registers
-          constexpr int kPB = C::kThreads > 512 ? 1 : (kOwn <= 1 ? 4 : (kOwn == 2 ? 2 : 1));
-          for (int cb = c_lo + 1; cb <= c_hi; cb += kPB) {
-            float pv[kPB][kOwn * 8];
-#pragma unroll
-            for (int u = 0; u < kPB; ++u) {
-              const float* pp = a.part + ((size_t)(cb + u + tile) * TMAX) * kTileN;
-#pragma unroll
-              for (int lc = 0; lc < kOwn; ++lc)
-#pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                  const int t = (kH * lc + h) * 8 + e;
-                  pv[u][lc * 8 + e] = (cb + u <= c_hi && t < a.T) ? __ldcg(pp + t * kTileN + r) : 0.f;
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < kPB; ++u)
-              if (cb + u <= c_hi)
-#pragma unroll
-                for (int k2 = 0; k2 < kOwn * 8; ++k2) acc[k2] = __fadd_rn(acc[k2], pv[u][k2]);
-          }
-        } else {
         // the owner's segment is its last one: the whole stage ring is drained and free
         float* const pst = reinterpret_cast<float*>(smem);
         constexpr int kRing = C::kStages * C::kStageBytes / 4;  // floats
@@ -1013,7 +868,6 @@ __device__ __forceinline__ void linear_body(const LinearArgs* __restrict__ A, co
           if (p0 + maxp < np) named_bar(1, kEpiT);  // before the next batch overwrites the ring
         }
         }
-        }
       }
       if (res_staged) {
         cp_async_wait_all();
@@ -1021,7 +875,7 @@ __device__ __forceinline__ void linear_body(const LinearArgs* __restrict__ A, co
       }
       if (QS_LIN_TIMELINE && a.dbg && et == 0) a.dbg[6144 + c] = gtimer();  // partials summed
       // ---------------------------------------------------------- post-ops
-      // one specialised tail per post-op class; a chain (OPC = kOpAny) dispatches once per tile
+      // the post-op class is a template parameter: a launch carries only its own tail
       auto post = [&](auto opc) {
         constexpr int OP = decltype(opc)::value;
         const bool valid = n < a.n;
@@ -1157,25 +1011,15 @@ __device__ __forceinline__ void linear_body(const LinearArgs* __restrict__ A, co
           }
         }
         if (QS_LIN_TIMELINE && a.dbg && et == 0) a.dbg[6656 + c] = gtimer();  // post-op stores issued
-        int* const sig = CHAIN && j + 1 < nlin ? ready + j + 1 : nullptr;  // chain: publish the emitted chunk
         if constexpr (OP == kOpStore) {
           if (a.emit == kEmitRms)
-            emit_rms<L, TMAX, kEpiT, C::kEpiWarps, CHAIN>(a, reinterpret_cast<float*>(smem + C::kStgOff), tile, et, sig);
+            emit_rms<L, TMAX, kEpiT, C::kEpiWarps>(a, reinterpret_cast<float*>(smem + C::kStgOff), tile, et);
         }
         if constexpr (OP == kOpSiluMul) {
-          if (a.emit == kEmitSilu) emit_silu<L, TMAX, kEpiT, C::kEpiWarps, CHAIN>(a, tile, et, flag, sig);
+          if (a.emit == kEmitSilu) emit_silu<L, TMAX, kEpiT, C::kEpiWarps>(a, tile, et, flag);
         }
       };
-      if constexpr (OPC == kOpAny) {
-        switch (a.op) {
-          case kOpSiluMul: post(std::integral_constant<int, kOpSiluMul>{}); break;
-          case kOpQkvRope: post(std::integral_constant<int, kOpQkvRope>{}); break;
-          case kOpLogits: post(std::integral_constant<int, kOpLogits>{}); break;
-          default: post(std::integral_constant<int, kOpStore>{}); break;
-        }
-      } else {
-        post(std::integral_constant<int, OPC>{});
-      }
+      post(std::integral_constant<int, OPC>{});
 #pragma unroll
       for (int t = 0; t < kOwn * 8; ++t) acc[t] = 0.f;
     }
@@ -1189,29 +1033,14 @@ __device__ __forceinline__ void linear_body(const LinearArgs* __restrict__ A, co
     tc_fence_after();
     tmem_dealloc<C::kTmemCols>(tmem);
   }
-  if (CHAIN && threadIdx.x == 0) {
-    // every CTA is past its last ready[] read: the last one out re-arms the chain counters
-    if (atomicAdd(exit_cnt, 1) == (int)gridDim.x - 1) {
-      for (int j = 1; j < nlin; ++j) ready[j] = 0;
-      *exit_cnt = 0;
-    }
-  }
   if (QS_LIN_TIMELINE && A[0].dbg && threadIdx.x == 0) A[0].dbg[2048 + c] = gtimer();
   ktrace_exit(A[0].kt);
 }
 
 template <int L, int TMAX, int OPC>
 __global__ void __launch_bounds__(LinCfg<L, TMAX>::kThreads, 1) linear_tc_kernel(const __grid_constant__ LinearArgs a) {
-  linear_body<L, TMAX, OPC, false>(&a, 1, nullptr, nullptr);
+  linear_body<L, TMAX, OPC>(&a);
 }
-
-template <int L, int TMAX>
-__global__ void __launch_bounds__(LinCfg<L, TMAX>::kThreads, 1)
-    linear_chain_kernel(const __grid_constant__ LinearChain ch) {
-  linear_body<L, TMAX, kOpAny, true>(ch.lin, ch.n, ch.ready, ch.exit_cnt);
-}
-
-
 
 template <int L, int TMAX, int OPC>
 static cudaError_t launch_linear_op(const LinearArgs& a, cudaStream_t st) {
@@ -1265,44 +1094,6 @@ cudaError_t launch_linear(int L, const LinearArgs& a, cudaStream_t st) {
     case 16: return launch_linear_t<3, 16>(a, st);
     case 32: return launch_linear_t<3, 32>(a, st);
     default: return launch_linear_t<3, 64>(a, st);
-  }
-}
-
-template <int L, int TMAX>
-static cudaError_t launch_chain_t(const LinearChain& ch, cudaStream_t st) {
-  using C = LinCfg<L, TMAX>;
-  static bool attr[kMaxDevices] = {};
-  int dev = 0;
-  cudaError_t e = cudaGetDevice(&dev);
-  if (e != cudaSuccess) return e;
-  if (dev >= kMaxDevices || !attr[dev]) {
-    e = cudaFuncSetAttribute(linear_chain_kernel<L, TMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             C::kSmemBytes);
-    if (e != cudaSuccess) return e;
-    if (dev < kMaxDevices) attr[dev] = true;
-  }
-  for (int j = 0; j < ch.n; ++j)
-    if (ch.lin[j].r_pad != C::kRowsMax || ch.lin[j].n_cta != ch.lin[0].n_cta) return cudaErrorInvalidValue;
-  return launch_k(linear_chain_kernel<L, TMAX>, dim3(ch.lin[0].n_cta), dim3(C::kThreads), C::kSmemBytes, st, ch);
-}
-
-// One launch for a chain of dependent linears (T <= 16 buckets).
-cudaError_t launch_linear_chain(int L, const LinearChain& ch, cudaStream_t st) {
-  if (ch.n < 1 || ch.n > kMaxChain) return cudaErrorInvalidValue;
-  const int tm = linear_tmax_bucket(ch.lin[0].T, L);
-  if (L == 1) {
-    switch (tm) {
-      case 8: return launch_chain_t<1, 8>(ch, st);
-      case 16: return launch_chain_t<1, 16>(ch, st);
-      default: return cudaErrorInvalidValue;
-    }
-  }
-  switch (tm) {
-    case 2: return launch_chain_t<3, 2>(ch, st);
-    case 4: return launch_chain_t<3, 4>(ch, st);
-    case 8: return launch_chain_t<3, 8>(ch, st);
-    case 16: return launch_chain_t<3, 16>(ch, st);
-    default: return cudaErrorInvalidValue;
   }
 }
 

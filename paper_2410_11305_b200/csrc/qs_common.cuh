@@ -87,8 +87,6 @@ struct KTraceScope {
 
 enum Emit : int { kEmitNone = 0, kEmitSilu = 1, kEmitRms = 2 };
 
-enum PostOpClass : int { kOpAny = -1 };  // kernel template: post-op chosen per linear at run time
-
 enum PostOp : int {
   kOpStore = 0,     // out[t, n] = y
   kOpResidual = 1,  // out[t, n] += y          (o_proj / down_proj)
@@ -192,20 +190,6 @@ struct LinearArgs {
 };
 
 
-
-// A chain of dependent linears in ONE persistent launch (T <= 16 forwards: o_proj ->
-// gate_up -> down_proj -> next q|k|v or lm_head).  Linear j+1's operand is emitted by
-// linear j's epilogue (LinearArgs::emit) and published through ready[j+1]: the weight
-// producer streams linear j+1's weights while linear j's fixups and emit finish; only the
-// activation copies wait for ready[j+1] == lin[j+1].n_chunks.  The last CTA out resets ready[] and
-// exit_cnt, so graph replays start from zero.
-constexpr int kMaxChain = 4;
-struct LinearChain {
-  LinearArgs lin[kMaxChain];
-  int n;
-  int* ready;     // [kMaxChain]: chunks of linear j's operand emitted so far (need: n_chunks)
-  int* exit_cnt;  // [1]
-};
 
 struct AttnArgs {
   const float* q;

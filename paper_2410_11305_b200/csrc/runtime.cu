@@ -15,7 +15,6 @@
 
 namespace qs {
 cudaError_t launch_linear(int L, const LinearArgs& a, cudaStream_t st);
-cudaError_t launch_linear_chain(int L, const LinearChain& ch, cudaStream_t st);
 int linear_tmax_bucket(int T, int L);
 cudaError_t launch_act_pack(int L, const PackArgs& a, cudaStream_t st);
 cudaError_t launch_attention(const AttnArgs& a, int n_blk, cudaStream_t st);
@@ -83,8 +82,6 @@ KTrace next_trace(int32_t tag) {
 constexpr int kMaxT = 64;
 constexpr int kGbarOffset = 4096;  // emit counters live past every per-tile counter
 constexpr int kEmitCnt = 8 + 1024;  // [0] arrive, [1] depart, [8 + q] per silu group
-constexpr int kChainOff = kGbarOffset + kEmitCnt + kMaxT * 128;  // chain ready[kMaxChain] + exit counter
-constexpr int kChainCnt = 8;
 
 int g_num_sms = 0;
 
@@ -407,8 +404,7 @@ int qs_workspace_size(const qs_model_t* m, int32_t t_max, qs_workspace_sizes_t* 
   out->ascale = 2 * (size_t)chunks * kMaxT * 4 * 5;  // two slots of ascale + acorr [n_chunks][a_ld][4]
   out->part = (size_t)(num_sms() + tiles) * kMaxT * kTileN * 4;
   // per-tile counters | emit counters [kGbarOffset, +8 + 1024) | emit leaf sums [kMaxT][<=128]
-  // | chain counters [8]
-  out->counters = (size_t)(kChainOff + kChainCnt) * 4;
+  out->counters = (size_t)(kGbarOffset + kEmitCnt + kMaxT * 128) * 4;
   if (tiles + 1 > kGbarOffset) return QS_ERR_SHAPE;
   out->arg_val = (size_t)wl.n_tiles * kMaxT * 4;
   out->arg_idx = (size_t)wl.n_tiles * kMaxT * 4;
@@ -601,12 +597,9 @@ void set_emit(LinearArgs& a, int kind, const qs_qweight_t& next, const Slot& sl,
   a.e_rotate = g_rotate;
   a.e_leaf = reinterpret_cast<float*>(ws->counters + kGbarOffset + kEmitCnt);
 }
-// fused next-operand emits (mask: 1 silu, 2 rmsnorm, 4 chained launches): -1 = QS_EMIT env,
-// default 3.  Chains (4) are bit-identical but measured slower: PDL already
-// hides the next linear's ramp, and the chained kernel's run-time argument indexing costs more.
-int g_emit = -1;
+int g_emit = -1;  // fused next-operand emits (mask: 1 silu, 2 rmsnorm): -1 = QS_EMIT env (default 3)
 int emit_mask() {
-  if (g_emit < 0) g_emit = env_int("QS_EMIT", 3) & 7;
+  if (g_emit < 0) g_emit = env_int("QS_EMIT", 3) & 3;
   return g_emit;
 }
 
@@ -677,10 +670,6 @@ int forward_impl(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const q
   int lin_j = 0;
   const int s0 = 0;            // slot read by qkv / gate_up / lm_head
   bool qkv_ready = false;      // qkv's operand already emitted by the previous down_proj
-  // Chained launches (LinearChain): with both emits on, o_proj -> gate_up -> down_proj ->
-  // next q|k|v (lm_head after the last layer) run as ONE persistent launch when every
-  // linear of the chain spans the whole grid (units >= #SMs).  Emit mask bit 4.
-  bool chained = false;        // this layer's qkv (or the lm_head) already ran in a chain
   auto qkv_args = [&](int li) {
     const qs_layer_t& ly = m->layers[li];
     // q|k|v projection; operand = rmsnorm(x) (+ embedding gather on layer 0), fused
@@ -727,7 +716,7 @@ int forward_impl(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const q
   };
   for (int li = 0; li < m->n_layers; ++li) {
     const qs_layer_t& ly = m->layers[li];
-    if (!chained) {
+    {
       LinearArgs a = qkv_args(li);
       ws_stream.window(a, lin_j++);
       if ((e = launch_linear_packed(L, a, st, mode * 16 + 0, !qkv_ready)) != cudaSuccess) return status(e);
@@ -794,49 +783,6 @@ int forward_impl(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const q
       set_emit(adn, kEmitRms, last ? m->lm_head : m->layers[li + 1].qkv, slot[s0],
                last ? m->final_norm : m->layers[li + 1].attn_norm, m->norm_eps, d, ws);
     ws_stream.window(adn, lin_j++);
-    LinearChain ch{};
-    if ((emit_mask() & 4) && emit_rms && emit_silu) {
-      ch.lin[0] = ao;
-      ch.lin[1] = agu;
-      ch.lin[2] = adn;
-      ch.lin[3] = last ? head_args() : qkv_args(li + 1);
-      ch.n = 4;
-      for (int j = 0; j < ch.n; ++j)
-        if (ch.lin[j].n_cta != num_sms()) ch.n = 0;
-    }
-    if (ch.n > 0) {
-      ws_stream.window(ch.lin[3], lin_j++);
-      ch.ready = ws->counters + kChainOff;
-      ch.exit_cnt = ws->counters + kChainOff + kMaxChain;
-      // o_proj's operand pack (attention merge + quantise), then the chain
-      prof_mark(st, mode * 16 + 5, true);  // kind 5: operand pack
-      ch.lin[0].pk.kt = next_trace(mode * 16 + 5);
-      if ((e = launch_act_pack(L, ch.lin[0].pk, st)) != cudaSuccess) return status(e);
-      prof_mark(st, 0, false);
-      g_launches += 2;
-      static const int split = env_int("QS_CHAIN_SPLIT", 0);  // experiment: one chain launch per linear
-      if (split) {
-        for (int j = 0; j < ch.n; ++j) {
-          LinearChain c1 = ch;
-          c1.lin[0] = ch.lin[j];
-          c1.n = 1;
-          c1.lin[0].kt = next_trace(mode * 16 + 7);
-          prof_mark(st, mode * 16 + 7, true);
-          if ((e = launch_linear_chain(L, c1, st)) != cudaSuccess) return status(e);
-          prof_mark(st, 0, false);
-        }
-        g_launches += ch.n - 1;
-      } else {
-      ch.lin[0].kt = next_trace(mode * 16 + 7);  // kind 7: chained o | gate_up | down | next
-      prof_mark(st, mode * 16 + 7, true);
-      if ((e = launch_linear_chain(L, ch, st)) != cudaSuccess) return status(e);
-      prof_mark(st, 0, false);
-      }
-      chained = true;
-      qkv_ready = true;
-      continue;
-    }
-    chained = false;
     if ((e = launch_linear_packed(L, ao, st, mode * 16 + 1)) != cudaSuccess) return status(e);
     if (tp) {
       const int rc = reduce_into_x();
@@ -850,7 +796,6 @@ int forward_impl(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const q
     }
     qkv_ready = emit_rms;
   }
-  if (chained) return QS_OK;  // the lm_head ran in the last chain (never under TP)
   LinearArgs a = head_args();
   ws_stream.window(a, lin_j++);
   e = launch_linear_packed(L, a, st, mode * 16 + 4, !qkv_ready);
@@ -877,7 +822,7 @@ int qs_forward_tp2(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const
 }
 
 int qs_set_emit(int32_t mask) {
-  g_emit = mask & 7;
+  g_emit = mask & 3;
   return QS_OK;
 }
 

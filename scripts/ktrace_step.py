@@ -19,7 +19,7 @@ import numpy as np
 
 sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
 
-KINDS = {0: "qkv", 1: "o", 2: "gate_up", 3: "down", 4: "lm_head", 5: "pack", 6: "attention", 7: "chain", 15: "linear"}
+KINDS = {0: "qkv", 1: "o", 2: "gate_up", 3: "down", 4: "lm_head", 5: "pack", 6: "attention", 15: "linear"}
 
 
 def main() -> None:
