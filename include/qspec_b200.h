@@ -122,6 +122,8 @@ typedef struct {
 const char* qs_version(void);
 int qs_num_sms(int32_t* out);
 int qs_linear_max_tokens(void); /* largest T one linear launch accepts (64) */
+int qs_attention_chunk_len(void); /* key positions per split-KV chunk (the attention grid covers
+                                     ceil(qs_batch_t.ctx_cap / this) chunks) */
 int qs_workspace_size(const qs_model_t* m, int32_t t_max, qs_workspace_sizes_t* out);
 int qs_qweight_geometry(int32_t n, int32_t k, int32_t g, qs_qweight_t* out); /* fills dims, not pointers */
 

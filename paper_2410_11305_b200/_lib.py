@@ -79,6 +79,7 @@ _SIGS = {
     "qs_version": ([], C.c_char_p),
     "qs_num_sms": ([C.POINTER(i32)], C.c_int),
     "qs_linear_max_tokens": ([], C.c_int),
+    "qs_attention_chunk_len": ([], C.c_int),
     "qs_workspace_size": ([C.POINTER(Model), i32, C.POINTER(WorkspaceSizes)], C.c_int),
     "qs_qweight_geometry": ([i32, i32, i32, C.POINTER(QWeight)], C.c_int),
     "qs_init_weight": ([u64, u64, f32, i32, i32, i32, vp, vp, i32, i32, i32, vp, vp, vp], C.c_int),

@@ -189,7 +189,7 @@ def measure_profile(model, batches: Sequence[int], ns: Sequence[int] = (1, 2, 4)
 
         def stage(per_seq):
             t["slot"][:B * per_seq].copy_(torch.arange(B, dtype=torch.int32, device="cuda").repeat_interleave(per_seq))
-            return eng._batches(per_seq)
+            return eng._batches(per_seq, ctx_cap=ctx + per_seq)   # every query sits at position ctx
 
         draft[B] = timed(stage(1), True)
         verify[B] = [(n, timed(stage(n), False)) for n in ns]

@@ -373,6 +373,7 @@ int qs_num_sms(int32_t* out) {
 }
 
 int qs_linear_max_tokens(void) { return kMaxT; }
+int qs_attention_chunk_len(void) { return attention_chunk_len(); }
 
 int qs_qweight_geometry(int32_t n, int32_t k, int32_t g, qs_qweight_t* out) {
   if (n < 1 || k < 1 || g < 1 || k % g != 0) return QS_ERR_CONFIG;

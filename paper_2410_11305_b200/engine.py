@@ -77,8 +77,17 @@ class DecodeEngine:
         self.draft_batches = self._batches(1)
         self.verify_batches = self._batches(G1)
         self.use_graphs = use_graphs
+        self.graphs: dict[int, object] = {}   # attention grid bound (ctx_cap) -> captured step
         self.graph = None
         self.n_launch_cycle = 0
+        # Host upper bound on max(committed) over the slots, kept without device reads:
+        # prefill sets it from the prompt length, a step adds at most gamma + 1 (qspec) or
+        # 1 (greedy) committed positions per slot, poll() tightens it to the exact value.
+        # The attention grid covers ceil(ctx_cap / chunk) key chunks; sizing ctx_cap from
+        # this bound instead of the KV capacity drops the CTAs past every sequence's context
+        # (at prompt 128, capacity 520: 9 chunk slots per (block, kv head), 3 in use).
+        self._ctx_hi = 0
+        self._page = _lib.load().qs_attention_chunk_len()
 
     def _setup_storage(self, model: TransformerModel, batch: int, gamma: int) -> None:
         """KV pool, workspace and the C model view the forwards run on (TP overrides)."""
@@ -95,8 +104,9 @@ class DecodeEngine:
         return argmax
 
     # ------------------------------------------------------------------ batches
-    def _batches(self, per_seq: int) -> list[tuple[_lib.Batch, int]]:
-        """qs_batch_t descriptors: sequences grouped so each forward has <= 64 tokens."""
+    def _batches(self, per_seq: int, ctx_cap: int | None = None) -> list[tuple[_lib.Batch, int]]:
+        """qs_batch_t descriptors: sequences grouped so each forward has <= 64 tokens.
+        ``ctx_cap`` bounds every query's context (pos + 1) in the batch (default: the KV capacity)."""
         import torch
         seqs_per = max(1, 64 // per_seq)
         out = []
@@ -109,7 +119,7 @@ class DecodeEngine:
             b = _lib.Batch(T=ns * per_seq, tokens=self.t["tok"].data_ptr() + off,
                            positions=self.t["pos"].data_ptr() + off, slots=self.t["slot"].data_ptr() + off,
                            n_blk=ns, blk_tok0=tok0.data_ptr(), blk_ntok=ntok.data_ptr(), blk_qmax=per_seq,
-                           ctx_cap=self.kv.capacity)
+                           ctx_cap=self.kv.capacity if ctx_cap is None else ctx_cap)
             out.append((b, off))
         return out
 
@@ -145,31 +155,65 @@ class DecodeEngine:
             self.step()
         return int(self._enq)
 
-    def step(self) -> None:
-        """One cycle (qspec) or one token (greedy) for every slot, replayed from a CUDA graph."""
+    def _advance(self) -> int:
+        """Committed positions one step can add per slot (accept commits <= g_eff + 1)."""
+        return self.gamma + 1 if self.algorithm == "qspec" else 1
+
+    def _ctx_cap(self, ctx_hi: int) -> int:
+        """Attention context bound of a step starting at max(committed) <= ctx_hi, rounded
+        up to whole key chunks (one captured graph per chunk count)."""
+        need = ctx_hi + self._advance()   # positions committed .. committed + gamma
+        c = self._page
+        return min(self.kv.capacity, -(-need // c) * c)
+
+    def _set_ctx_cap(self, cap: int) -> None:
+        for b, _ in self.draft_batches + self.verify_batches:
+            b.ctx_cap = cap
+
+    def _capture(self, cap: int, warm: bool) -> None:
+        """Capture the step body for attention bound ``cap``.  Warm-up (sets kernel
+        attributes outside capture) and capture run with every slot marked done: the
+        accept/commit kernels skip done slots, so the only side effects are scratch
+        buffers and KV rows past committed_len, which the next real cycle rewrites
+        before reading."""
         import torch
         body = self._cycle_body if self.algorithm == "qspec" else self._ar_body
-        if not self.use_graphs:
-            body()
-            return
-        if self.graph is None:
-            # Warm-up (sets kernel attributes outside capture) and capture run with every
-            # slot marked done: the accept/commit kernels skip done slots, so the only
-            # side effects are scratch buffers and KV rows past committed_len, which the
-            # next real cycle rewrites before reading.
-            done = self.t["done"].clone()
-            self.t["done"].fill_(1)
+        self._set_ctx_cap(cap)
+        done = self.t["done"].clone()
+        self.t["done"].fill_(1)
+        if warm:
             s = torch.cuda.Stream()
             s.wait_stream(torch.cuda.current_stream())
             with torch.cuda.stream(s):
                 body()
             torch.cuda.current_stream().wait_stream(s)
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
-                body()
-            torch.cuda.synchronize()
-            self.t["done"].copy_(done)
-            self.graph = g
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            body()
+        torch.cuda.synchronize()
+        self.t["done"].copy_(done)
+        self.graphs[cap] = g
+
+    def step(self) -> None:
+        """One cycle (qspec) or one token (greedy) for every slot, replayed from a CUDA graph
+        (one graph per attention context bound; the next few bounds are captured ahead so a
+        run of steps does not stop to capture)."""
+        body = self._cycle_body if self.algorithm == "qspec" else self._ar_body
+        cap = self._ctx_cap(self._ctx_hi)
+        self._ctx_hi += self._advance()
+        if not self.use_graphs:
+            self._set_ctx_cap(cap)
+            body()
+            return
+        if cap not in self.graphs:
+            self._capture(cap, warm=not self.graphs)
+            nxt = cap
+            for _ in range(3):
+                nxt = self._ctx_cap(nxt)
+                if nxt not in self.graphs:
+                    self._capture(nxt, warm=False)
+            self._set_ctx_cap(cap)
+        self.graph = self.graphs[cap]
         self.graph.replay()
 
     def profile_step(self) -> list[tuple[float, int]]:
@@ -182,6 +226,8 @@ class DecodeEngine:
         body = self._cycle_body if self.algorithm == "qspec" else self._ar_body
         if self.graph is None:
             self.step()           # ensures warm-up happened (attributes set)
+        self._set_ctx_cap(self._ctx_cap(self._ctx_hi))
+        self._ctx_hi += self._advance()
         n_max = 8192
         _lib.call("qs_profile_enable", n_max)
         g = torch.cuda.CUDAGraph()
@@ -206,6 +252,8 @@ class DecodeEngine:
         body = self._cycle_body if self.algorithm == "qspec" else self._ar_body
         if self.graph is None:
             self.step()
+        self._set_ctx_cap(self._ctx_cap(self._ctx_hi))
+        self._ctx_hi += self._advance()
         cap = 16384
         buf = torch.zeros((cap, 2), dtype=torch.int64, device="cuda")
         _lib.call("qs_ktrace_enable", buf.data_ptr(), cap)
@@ -243,6 +291,7 @@ class DecodeEngine:
                 raise TokenIdError("prompt token out of vocab range")
             prompt = [int(t) for t in prompt]
         low = self.algorithm == "greedy" and self.greedy_low
+        self._ctx_hi = max(self._ctx_hi, len(prompt))
         argmax = self._prefill_argmax(prompt, slot, low)
         first = argmax[len(prompt) - 1:len(prompt)]
         b = slot
@@ -262,8 +311,21 @@ class DecodeEngine:
         else:
             self.t["done"][b] = 0
 
+    def poll(self) -> bool:
+        """Host read of the done flags (and committed lengths, which tighten the attention
+        context bound): True when every slot is done."""
+        import torch
+        if getattr(self, "_poll_buf", None) is None:
+            self._poll_buf = torch.empty(2 * self.B, dtype=torch.int32).pin_memory()
+        h = self._poll_buf
+        h[:self.B].copy_(self.t["done"], non_blocking=True)
+        h[self.B:].copy_(self.t["committed"], non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        self._ctx_hi = int(h[self.B:].max())
+        return bool(h[:self.B].all())
+
     def all_done(self) -> bool:
-        return bool(self.t["done"].all().item())
+        return self.poll()
 
     def run(self, max_steps: int = 1 << 30, poll: int = 1) -> int:
         steps = 0

@@ -171,3 +171,31 @@ def test_cycle_accounting():
         assert 1 <= len(rec.emitted) <= 5 and rec.accept_len <= len(rec.drafted)
     txt = Q.format_trace(r.cycles)
     assert len(Q.parse_trace(txt)) == len(r.cycles)
+
+
+@pytest.mark.parametrize("algorithm", ["qspec", "greedy"])
+def test_attention_context_bound_matches_full_grid(algorithm):
+    """The engine sizes the attention grid from a host bound on the committed lengths
+    (engine._ctx_cap); runs crossing several 64-key chunk boundaries, with and without
+    poll() tightening the bound mid-run, give the tokens and per-cycle traces of a run over
+    the full KV capacity."""
+    m = toy(9, vocab_size=512, max_seq_len=320)
+    prompts = [[3, 1, 4, 1, 5] * 12, [2, 7], [9] * 130]
+    runs = []
+    for mode in ("full", "bound", "bound_nopoll"):
+        eng = DecodeEngine(m, 3, gamma=3, max_new_cap=160, algorithm=algorithm)
+        if mode == "full":
+            eng._ctx_cap = lambda hi, e=eng: e.kv.capacity
+        for b, p in enumerate(prompts):
+            eng.prefill(b, p, 150)
+        if mode == "bound_nopoll":
+            for _ in range(200):
+                eng.step()
+            assert eng.all_done()
+        else:
+            eng.run()
+        caps = sorted(eng.graphs)
+        runs.append(([eng.result(b).new_tokens for b in range(3)], [eng.result(b).trace.tolist() for b in range(3)]))
+        if mode != "full":
+            assert len(caps) > 1 and min(caps) < eng.kv.capacity, caps
+    assert runs[1] == runs[0] and runs[2] == runs[0]
