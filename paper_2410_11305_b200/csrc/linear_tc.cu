@@ -227,12 +227,17 @@ __device__ __forceinline__ bool op_is(const LinearArgs& a) {
 // splits down to 128-element leaves, each summed with 8 strided accumulators and the
 // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) bracket; leaves combine as a balanced tree
 // (token_inv_rms in pack_dev.cuh states the same order).
+// Each leaf is published as ~bits(sum) into a zero-cleared slot, so the owners wait for
+// their tokens' leaves by polling the leaves themselves: the last owner's publish reaches
+// every owner in one round trip (no counter barrier followed by a second round of loads).
 template <int L, int TMAX, int kEpiT, int kEpiWarps>
 __device__ __forceinline__ void emit_rms(const LinearArgs& a, float* stg, int tile, int et) {
   const int lane = et & 31, ew = et >> 5;
   constexpr int kTW = (TMAX + kEpiWarps - 1) / kEpiWarps;  // tokens per warp
-  // this tile's RMSNorm weights do not depend on the barrier: in flight across it
+  // this tile's RMSNorm weights do not depend on the leaves: in flight across the wait
   const float4 wv = *reinterpret_cast<const float4*>(a.e_rms_w + (size_t)tile * 128 + 4 * lane);
+  // clear this tile's column of the other leaf buffer (its readers' launch has completed)
+  for (int t = et; t < kLeafRows; t += kEpiT) a.e_leaf_clr[t * kLeafLd + tile] = 0u;
   named_bar(1, kEpiT);
   for (int base = 0; base < a.T * 8; base += kEpiT) {
     const int item = base + et, t = item >> 3, j = item & 7;
@@ -247,31 +252,35 @@ __device__ __forceinline__ void emit_rms(const LinearArgs& a, float* stg, int ti
     rs = __fadd_rn(rs, __shfl_xor_sync(0xffffffffu, rs, 1));
     rs = __fadd_rn(rs, __shfl_xor_sync(0xffffffffu, rs, 2));
     rs = __fadd_rn(rs, __shfl_xor_sync(0xffffffffu, rs, 4));
-    if (on && j == 0) __stcg(a.e_leaf + (size_t)t * a.n_tiles + tile, rs);
+    // ~bits is never 0: sums of squares are >= +0 or a NaN other than 0xffffffff
+    if (on && j == 0) st_relaxed_u32(a.e_leaf + t * kLeafLd + tile, ~__float_as_uint(rs));
   }
-  // bar.sync then ONE gpu-scope release by et 0: cumulative over the CTA's leaf writes
-  named_bar(1, kEpiT);
-  if (et == 0) {
-    red_release_add(&a.e_cnt[0], 1);
+  float* inv = stg + 128 * (a.T > 8 ? a.T : 8);
+  const int nl = a.n_tiles, per = nl > 32 ? nl >> 5 : 1, lanes = nl > 32 ? 32 : nl;
+  // every leaf of this warp's tokens polled at once until all are published
+  float s[kTW][4];
+  {
     const unsigned long long t0 = gtimer();
-    while (ld_acquire(&a.e_cnt[0]) < a.n_tiles) {
+    for (;;) {
+      bool ok = true;
+#pragma unroll
+      for (int k = 0; k < kTW; ++k) {
+        const int t = ew + k * kEpiWarps;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          s[k][i] = 0.f;
+          if (t < a.T && i < per && lane * per + i < nl) {
+            const unsigned w = ld_relaxed_u32(a.e_leaf + t * kLeafLd + lane * per + i);
+            ok = ok && w != 0u;
+            s[k][i] = __uint_as_float(~w);
+          }
+        }
+      }
+      if (__all_sync(0xffffffffu, ok)) break;
       if (gtimer() - t0 > 5000000000ull) __trap();
     }
   }
-  named_bar(1, kEpiT);
-  if (QS_LIN_TIMELINE && a.dbg && et == 0) a.dbg[7168 + blockIdx.x] = gtimer();  // owner barrier passed
-  float* inv = stg + 128 * (a.T > 8 ? a.T : 8);
-  const int nl = a.n_tiles, per = nl > 32 ? nl >> 5 : 1, lanes = nl > 32 ? 32 : nl;
-  // every leaf load of this warp's tokens in flight at once, then the pairwise sums
-  float s[kTW][4];
-#pragma unroll
-  for (int k = 0; k < kTW; ++k) {
-    const int t = ew + k * kEpiWarps;
-    const float* lf = a.e_leaf + (size_t)t * nl;
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-      s[k][i] = (t < a.T && i < per && lane * per + i < nl) ? __ldcg(lf + lane * per + i) : 0.f;
-  }
+  if (QS_LIN_TIMELINE && a.dbg && et == 0) a.dbg[7168 + blockIdx.x] = gtimer();  // every leaf seen
 #pragma unroll
   for (int k = 0; k < kTW; ++k) {
     const int t = ew + k * kEpiWarps;
@@ -288,7 +297,7 @@ __device__ __forceinline__ void emit_rms(const LinearArgs& a, float* stg, int ti
       inv[t] = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(ms, a.e_eps)));
     }
   }
-  named_bar(1, kEpiT);
+  __syncwarp();  // inv[t] of this warp's tokens: written and read by this warp only
   if (QS_LIN_TIMELINE && a.dbg && et == 0) a.dbg[7936 + blockIdx.x] = gtimer();  // 1/rms known
   // rolled on purpose: the tail runs once per owner with a cold instruction cache, and
   // one loop body fetched once beats kTW unrolled copies (measured: down_proj T=16 emit
@@ -304,12 +313,6 @@ __device__ __forceinline__ void emit_rms(const LinearArgs& a, float* stg, int ti
     quant_group_warp<L>(v, t, tile, lane, a.e_img, a.e_ascale, a.e_acorr, a.r_pad, a.a_ld, a.e_rotate != 0);
   }
   if (QS_LIN_TIMELINE && a.dbg && et == 0) a.dbg[7680 + blockIdx.x] = gtimer();  // quantised
-  if (et == 0) {  // the last owner through resets both counters (every owner is past the wait)
-    if (atomicAdd(&a.e_cnt[1], 1) == a.n_tiles - 1) {
-      a.e_cnt[0] = 0;
-      a.e_cnt[1] = 0;
-    }
-  }
 }
 
 // kEmitSilu (gate_up): tiles 2q, 2q+1 hold silu outputs 128q..128q+127 = group q of

@@ -47,7 +47,9 @@ inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
-constexpr int kMaxDevices = 64;  // per-device caches of kernel attributes
+constexpr int kMaxDevices = 64;
+constexpr int kLeafLd = 128;    // emit leaf-sum row stride (d_model tiles <= 128)
+constexpr int kLeafRows = 64;   // emit leaf-sum rows (tokens) cleared per tile  // per-device caches of kernel attributes
 constexpr int kTileN = 128;    // output rows per tile (UMMA M)
 constexpr int kChunkK = 128;   // K positions per chunk (one SW128 row of int8)
 constexpr int kChunkBytes = kTileN * kChunkK / 2;  // 8 KiB packed weights per (tile, chunk)
@@ -181,8 +183,12 @@ struct LinearArgs {
   const float* e_rms_w;
   float e_eps;
   int e_n;         // row width (the RMSNorm mean's n)
-  float* e_leaf;   // [T][n_tiles]
-  int* e_cnt;      // [0] arrive, [1] depart (kEmitRms); [8 + q] per group (kEmitSilu); zero on entry and exit
+  // kEmitRms leaf sums, [t][kLeafLd] as ~bits(sum) (0 = not yet published): o_proj and
+  // down_proj alternate between two buffers, each launch clearing the other one's entries
+  // of its tiles (that buffer's last readers belong to a launch that has completed)
+  unsigned* e_leaf;
+  unsigned* e_leaf_clr;
+  int* e_cnt;      // [8 + q] per group (kEmitSilu); zero on entry and exit
   int e_rotate;    // Hadamard-rotate the emitted groups (model option)
   // debug timeline (CTA 0): [role][i] globaltimer ns; roles: 0 producer issue, 1 unpack done,
   // 2 mma issued, 3 epilogue start (acc ready), 4 epilogue done

@@ -80,6 +80,7 @@ KTrace next_trace(int32_t tag) {
 }
 
 constexpr int kMaxT = 64;
+static_assert(kMaxT <= kLeafRows, "emit leaf rows cover every token of a forward");
 constexpr int kGbarOffset = 4096;  // emit counters live past every per-tile counter
 constexpr int kEmitCnt = 8 + 1024;  // [0] arrive, [1] depart, [8 + q] per silu group
 
@@ -404,8 +405,8 @@ int qs_workspace_size(const qs_model_t* m, int32_t t_max, qs_workspace_sizes_t* 
   out->img = 2 * (size_t)chunks * img_rows(kMaxT, 3) * 128;  // two operand slots (emit double buffer)
   out->ascale = 2 * (size_t)chunks * kMaxT * 4 * 5;  // two slots of ascale + acorr [n_chunks][a_ld][4]
   out->part = (size_t)(num_sms() + tiles) * kMaxT * kTileN * 4;
-  // per-tile counters | emit counters [kGbarOffset, +8 + 1024) | emit leaf sums [kMaxT][<=128]
-  out->counters = (size_t)(kGbarOffset + kEmitCnt + kMaxT * 128) * 4;
+  // per-tile counters | emit counters [kGbarOffset, +8 + 1024) | 2 x emit leaf sums [64][128]
+  out->counters = (size_t)(kGbarOffset + kEmitCnt + 2 * kLeafRows * kLeafLd) * 4;
   if (tiles + 1 > kGbarOffset) return QS_ERR_SHAPE;
   out->arg_val = (size_t)wl.n_tiles * kMaxT * 4;
   out->arg_idx = (size_t)wl.n_tiles * kMaxT * 4;
@@ -586,7 +587,7 @@ void use_slot(LinearArgs& a, const qs_qweight_t& w, const Slot& sl) {
   a.pk.acorr = reinterpret_cast<int32_t*>(sl.ascale + (size_t)w.n_chunks * a.pk.a_ld);
 }
 void set_emit(LinearArgs& a, int kind, const qs_qweight_t& next, const Slot& sl, const float* rms_w, float eps,
-              int n, const qs_workspace_t* ws) {
+              int n, const qs_workspace_t* ws, int leaf_buf = 0) {
   a.emit = kind;
   a.e_img = sl.img;
   a.e_ascale = sl.ascale;
@@ -596,7 +597,9 @@ void set_emit(LinearArgs& a, int kind, const qs_qweight_t& next, const Slot& sl,
   a.e_n = n;
   a.e_cnt = ws->counters + kGbarOffset;
   a.e_rotate = g_rotate;
-  a.e_leaf = reinterpret_cast<float*>(ws->counters + kGbarOffset + kEmitCnt);
+  unsigned* leaves = reinterpret_cast<unsigned*>(ws->counters + kGbarOffset + kEmitCnt);
+  a.e_leaf = leaves + leaf_buf * kLeafRows * kLeafLd;
+  a.e_leaf_clr = leaves + (leaf_buf ^ 1) * kLeafRows * kLeafLd;
 }
 int g_emit = -1;  // fused next-operand emits (mask: 1 silu, 2 rmsnorm): -1 = QS_EMIT env (default 3)
 int emit_mask() {
@@ -782,7 +785,7 @@ int forward_impl(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const q
     const bool last = li + 1 == m->n_layers;
     if (emit_rms)
       set_emit(adn, kEmitRms, last ? m->lm_head : m->layers[li + 1].qkv, slot[s0],
-               last ? m->final_norm : m->layers[li + 1].attn_norm, m->norm_eps, d, ws);
+               last ? m->final_norm : m->layers[li + 1].attn_norm, m->norm_eps, d, ws, 1);
     ws_stream.window(adn, lin_j++);
     if ((e = launch_linear_packed(L, ao, st, mode * 16 + 1)) != cudaSuccess) return status(e);
     if (tp) {
