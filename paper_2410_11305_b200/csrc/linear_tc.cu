@@ -231,11 +231,9 @@ __device__ __forceinline__ bool op_is(const LinearArgs& a) {
 // their tokens' leaves by polling the leaves themselves: the last owner's publish reaches
 // every owner in one round trip (no counter barrier followed by a second round of loads).
 template <int L, int TMAX, int kEpiT, int kEpiWarps>
-__device__ __forceinline__ void emit_rms(const LinearArgs& a, float* stg, int tile, int et) {
+__device__ __forceinline__ void emit_rms(const LinearArgs& a, float* stg, int tile, int et, int* pending) {
   const int lane = et & 31, ew = et >> 5;
   constexpr int kTW = (TMAX + kEpiWarps - 1) / kEpiWarps;  // tokens per warp
-  // this tile's RMSNorm weights do not depend on the leaves: in flight across the wait
-  const float4 wv = *reinterpret_cast<const float4*>(a.e_rms_w + (size_t)tile * 128 + 4 * lane);
   // clear this tile's column of the other leaf buffer (its readers' launch has completed)
   for (int t = et; t < kLeafRows; t += kEpiT) a.e_leaf_clr[t * kLeafLd + tile] = 0u;
   named_bar(1, kEpiT);
@@ -297,22 +295,27 @@ __device__ __forceinline__ void emit_rms(const LinearArgs& a, float* stg, int ti
       inv[t] = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(ms, a.e_eps)));
     }
   }
-  __syncwarp();  // inv[t] of this warp's tokens: written and read by this warp only
   if (QS_LIN_TIMELINE && a.dbg && et == 0) a.dbg[7936 + blockIdx.x] = gtimer();  // 1/rms known
-  // rolled on purpose: the tail runs once per owner with a cold instruction cache, and
-  // one loop body fetched once beats kTW unrolled copies (measured: down_proj T=16 emit
-  // 4.9 -> 3.0 us from the owner barrier to the quantised chunk)
+  // the group quantiser runs after the CTA's final barrier, spread over all warps
+  // (emit_rms_quantise): every other role is idle by then
+  if (et == 0) *pending = tile + 1;
+}
+
+// The owned tile's group of the RMSNorm'd rows, one token per warp of the whole CTA (the
+// tile is the owner's last segment, so this is the CTA's last work).
+template <int L>
+__device__ __forceinline__ void emit_rms_quantise(const LinearArgs& a, const float* stg, int tile, int warp,
+                                                  int nwarps, int lane) {
+  const float4 wv = *reinterpret_cast<const float4*>(a.e_rms_w + (size_t)tile * 128 + 4 * lane);
+  const float* inv = stg + 128 * (a.T > 8 ? a.T : 8);
 #pragma unroll 1
-  for (int k = 0; k < kTW; ++k) {
-    const int t = ew + k * kEpiWarps;
-    if (t >= a.T) break;
+  for (int t = warp; t < a.T; t += nwarps) {
     const float iv = inv[t];
     const float4 xv = *reinterpret_cast<const float4*>(stg + t * 128 + 4 * lane);
     const float v[4] = {__fmul_rn(__fmul_rn(xv.x, iv), wv.x), __fmul_rn(__fmul_rn(xv.y, iv), wv.y),
                         __fmul_rn(__fmul_rn(xv.z, iv), wv.z), __fmul_rn(__fmul_rn(xv.w, iv), wv.w)};
     quant_group_warp<L>(v, t, tile, lane, a.e_img, a.e_ascale, a.e_acorr, a.r_pad, a.a_ld, a.e_rotate != 0);
   }
-  if (QS_LIN_TIMELINE && a.dbg && et == 0) a.dbg[7680 + blockIdx.x] = gtimer();  // quantised
 }
 
 // kEmitSilu (gate_up): tiles 2q, 2q+1 hold silu outputs 128q..128q+127 = group q of
@@ -365,6 +368,7 @@ __device__ __forceinline__ void linear_body(const LinearArgs* __restrict__ A) {
   float* sring = reinterpret_cast<float*>(smem + C::kScaleOff);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::kNumBars);
   int* flag = reinterpret_cast<int*>(tmem_slot + 2);
+  int* emit_pending = reinterpret_cast<int*>(tmem_slot + 3);  // kEmitRms: owned tile + 1, quantised at exit
   float* red_val = reinterpret_cast<float*>(tmem_slot + 4);  // [4][TMAX]
   int* red_idx = reinterpret_cast<int*>(red_val + 4 * TMAX);  // [4][TMAX]
 
@@ -391,6 +395,7 @@ __device__ __forceinline__ void linear_body(const LinearArgs* __restrict__ A) {
     }
     for (int i = 0; i < C::kSStages; ++i) { mbar_init(&sfull[i], 1); mbar_init(&sempty[i], C::kEpiWarps); }
     if (C::kPref) mbar_init(pbar, 1);
+    *emit_pending = 0;
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc<C::kTmemCols>(tmem_slot);
@@ -1016,7 +1021,8 @@ __device__ __forceinline__ void linear_body(const LinearArgs* __restrict__ A) {
         if (QS_LIN_TIMELINE && a.dbg && et == 0) a.dbg[6656 + c] = gtimer();  // post-op stores issued
         if constexpr (OP == kOpStore) {
           if (a.emit == kEmitRms)
-            emit_rms<L, TMAX, kEpiT, C::kEpiWarps>(a, reinterpret_cast<float*>(smem + C::kStgOff), tile, et);
+            emit_rms<L, TMAX, kEpiT, C::kEpiWarps>(a, reinterpret_cast<float*>(smem + C::kStgOff), tile, et,
+                                                   emit_pending);
         }
         if constexpr (OP == kOpSiluMul) {
           if (a.emit == kEmitSilu) emit_silu<L, TMAX, kEpiT, C::kEpiWarps>(a, tile, et, flag);
@@ -1035,6 +1041,13 @@ __device__ __forceinline__ void linear_body(const LinearArgs* __restrict__ A) {
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc<C::kTmemCols>(tmem);
+  }
+  if constexpr (OPC == kOpStore) {
+    if (*emit_pending) {
+      emit_rms_quantise<L>(A[0], reinterpret_cast<const float*>(smem + C::kStgOff), *emit_pending - 1, warp,
+                           C::kThreads / 32, lane);
+      if (QS_LIN_TIMELINE && A[0].dbg && threadIdx.x == 0) A[0].dbg[7680 + c] = gtimer();  // quantised
+    }
   }
   if (QS_LIN_TIMELINE && A[0].dbg && threadIdx.x == 0) A[0].dbg[2048 + c] = gtimer();
   ktrace_exit(A[0].kt);
