@@ -165,7 +165,10 @@ __device__ __forceinline__ void reg_dep(uint32_t (&r)[N]) {
   for (int i = 0; i < N; ++i) asm volatile("" : "+r"(r[i]));
 }
 
-__device__ __forceinline__ long long umul_div(long long a, long long b, long long c) { return a * b / c; }
+// 32-bit unsigned: a * b < 2^31 for every launch (launch_linear checks n_units * n_cta);
+// a 64-bit division is a ~70-instruction dependent chain and the segment-end lookups
+// below sit on the owners' critical path
+__device__ __forceinline__ unsigned umul_div(unsigned a, unsigned b, unsigned c) { return a * b / c; }
 
 // CTA c of P covers units [bnd(c), bnd(c+1)) of U = n_tiles * n_chunks.
 __device__ __forceinline__ int unit_bound(int c, int U, int P) { return (int)umul_div(c, U, P); }
@@ -1095,6 +1098,7 @@ int linear_tmax_bucket(int T, int L) {
 
 cudaError_t launch_linear(int L, const LinearArgs& a, cudaStream_t st) {
   const int tm = linear_tmax_bucket(a.T, L);
+  if ((long long)a.n_tiles * a.n_chunks * (a.n_cta + 1) >= (1ll << 31)) return cudaErrorInvalidValue;  // umul_div range
   if (L == 1) {
     switch (tm) {
       case 8: return launch_linear_t<1, 8>(a, st);
