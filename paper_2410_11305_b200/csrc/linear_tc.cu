@@ -382,12 +382,36 @@ __device__ __forceinline__ void linear_body(const LinearArgs* __restrict__ A) {
   ktrace_enter(A[0].kt);
   pdl_launch_dependents();
 
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < C::kStages; ++i) {
-      mbar_init(&wfull[i], 1);
-      mbar_init(&afull[i], 1);
-      mbar_init(&empty[i], 1);
+  // Warp 0 initialises the weight-ring barriers and requests the first stages of weights
+  // (independent of the previous kernel) BEFORE the CTA-wide barrier, so a CTA that enters
+  // late -- its SM was held by one of the predecessor's owners -- starts its HBM stream
+  // without waiting for the other roles' set-up and the TMEM allocation.
+  int w_npro = 0;  // warp 0: weight stages already requested
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int i = 0; i < C::kStages; ++i) {
+        mbar_init(&wfull[i], 1);
+        mbar_init(&afull[i], 1);
+        mbar_init(&empty[i], 1);
+      }
+      fence_mbar_init();
     }
+    __syncwarp();
+    const LinearArgs& a = A[0];
+    const int NC = a.n_chunks, U = a.n_tiles * NC, P = a.n_cta;
+    StageIt it{unit_bound(c, U, P), unit_bound(c + 1, U, P), NC, CPS};
+    for (; w_npro < C::kStages && it.next(); ++w_npro) {
+      uint8_t* st = smem + w_npro * C::kStageBytes;
+      if (QS_AB & 16) {
+        if (lane == 0) mbar_arrive(&wfull[w_npro]);
+      } else {
+        mbar_arrive_expect_tx_elect(&wfull[w_npro], (uint32_t)it.nq * kChunkBytes);
+        bulk_g2s_elect(st, a.codes + ((size_t)it.tile * NC + it.ch0) * kChunkBytes, it.nq * kChunkBytes,
+                       &wfull[w_npro]);
+      }
+    }
+  }
+  if (threadIdx.x == 32) {
     for (int i = 0; i < C::kASlots; ++i) {
       mbar_init(&tfull[i], 4);
       mbar_init(&tempty[i], 1);
@@ -423,17 +447,8 @@ __device__ __forceinline__ void linear_body(const LinearArgs* __restrict__ A) {
       QS_LIN_GEOM(0)
       const uint32_t act_bytes = (uint32_t)a.r_pad * 128u;
       StageIt it{u0, u1, NC, CPS};
-      int npro = 0;
-      for (; npro < C::kStages && it.next(); ++npro) {
-        uint8_t* st = smem + npro * C::kStageBytes;
-        if (QS_AB & 16) {
-          if (lane == 0) mbar_arrive(&wfull[npro]);
-        } else {
-          mbar_arrive_expect_tx_elect(&wfull[npro], (uint32_t)it.nq * kChunkBytes);
-          bulk_g2s_elect(st, a.codes + ((size_t)it.tile * NC + it.ch0) * kChunkBytes, it.nq * kChunkBytes,
-                         &wfull[npro]);
-        }
-      }
+      const int npro = w_npro;  // requested before the CTA barrier
+      for (int k = 0; k < npro; ++k) it.next();
       // L2 prefetch (no smem, no barrier): the rest of this CTA's own weight range, then
       // its share of the forward's look-ahead window (later linears' weights)
       if (lane == 0) {
