@@ -83,7 +83,8 @@ typedef struct {
   const int32_t* positions; /* device [T] absolute positions */
   const int32_t* slots;     /* device [T] KV slot (block-table row) */
   int32_t n_blk;
-  const int32_t* blk_tok0;  /* device [n_blk] */
+  const int32_t* blk_tok0;  /* device [n_blk]; NULL (with blk_ntok NULL): uniform blocks, block i =
+                               tokens [i * blk_qmax, (i + 1) * blk_qmax) */
   const int32_t* blk_ntok;  /* device [n_blk] */
   int32_t blk_qmax;         /* max tokens per block (<= 64 / (n_heads/n_kv_heads)) */
   int32_t ctx_cap;          /* max context any query can see */

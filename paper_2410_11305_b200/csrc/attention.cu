@@ -80,7 +80,8 @@ __global__ void __launch_bounds__(256) attn_partial_kernel(const AttnArgs a) {
   const int blk = blockIdx.x, kvh = blockIdx.y, ch = blockIdx.z, tid = threadIdx.x;
   // the prologue is a chain of dependent global round trips: block -> positions + slot
   // -> page table -> K / V rows; each level's loads are issued together
-  const int ntok = a.blk_ntok[blk], tok0 = a.blk_tok0[blk];
+  // uniform blocks (blk_tok0 == nullptr, the decode engine's batches): no block-table load
+  const int ntok = a.blk_tok0 ? a.blk_ntok[blk] : a.qmax, tok0 = a.blk_tok0 ? a.blk_tok0[blk] : blk * a.qmax;
   if (ntok <= 0) return;
   const int j0 = ch * kAttnChunk;
   const int sl = a.slot[tok0];
@@ -116,7 +117,8 @@ __global__ void __launch_bounds__(256) attn_partial_kernel(const AttnArgs a) {
       mbar_arrive_expect_tx(&kv_bar[1], bytes);
     }
     __syncwarp();
-    const int p_first = j0 / a.page, p_last = (j0 + nk - 1) / a.page;
+    const int ps = __ffs(a.page) - 1;  // page is a power of two (qs_forward checks)
+    const int p_first = j0 >> ps, p_last = (j0 + nk - 1) >> ps;
     for (int pi = p_first + lane; pi <= p_last; pi += 32) {
       const int r0 = max(j0, pi * a.page), r1 = min(j0 + nk, (pi + 1) * a.page);
       const size_t off = (((size_t)bt[pi] * a.KV + kvh) * a.page + (r0 - pi * a.page)) * hd;
@@ -126,8 +128,9 @@ __global__ void __launch_bounds__(256) attn_partial_kernel(const AttnArgs a) {
     }
   }
   const int hd4 = hd >> 2;
+  const int hs = (hd >= 4 && (hd & (hd - 1)) == 0) ? __ffs(hd) - 1 : -1;  // head_dim shift (power of two)
   for (int e = tid; e < Q * hd4; e += blockDim.x) {
-    const int qi = e / hd4, d4 = e - qi * hd4;
+    const int qi = hs >= 0 ? e >> (hs - 2) : e / hd4, d4 = e - qi * hd4;
     const int i = qi / hpk, h = kvh * hpk + qi % hpk;
     cp_async16(qv + qi * hd + d4 * 4, a.q + (size_t)(tok0 + i) * a.ldq + (size_t)h * hd + d4 * 4);
   }
@@ -192,7 +195,7 @@ __global__ void __launch_bounds__(256) attn_partial_kernel(const AttnArgs a) {
   // ---- o_c = sum_j p_j v_j  (thread per (query, dim))
   mbar_wait(&kv_bar[1], 0);
   for (int e = tid; e < Q * hd; e += blockDim.x) {
-    const int qi = e / hd, d = e - qi * hd;
+    const int qi = hs >= 0 ? e >> hs : e / hd, d = e - qi * hd;
     const float* p = sc + qi * kAttnChunk;
     float acc = 0.f;
     for (int jj = 0; jj < nk; ++jj) acc = fmaf(p[jj], vt[jj * hd + d], acc);

@@ -920,7 +920,7 @@ __device__ __forceinline__ void linear_body(const LinearArgs* __restrict__ A) {
   #pragma unroll
         for (int lc = 0; lc < kOwn; ++lc) {
           float pc[8], ps[8];  // qkv: cos / sin of the chunk's 8 tokens
-          int pr[8];           // qkv: KV page * page_len + in-page row
+          int pr[8], prow[8];  // qkv: KV page and in-page row
           if constexpr (OP == kOpQkvRope) {
             const bool is_v = n >= a.n_q + a.n_k;
             const int loc = n < a.n_q ? n : (is_v ? n - a.n_q - a.n_k : n - a.n_q);
@@ -937,8 +937,10 @@ __device__ __forceinline__ void linear_body(const LinearArgs* __restrict__ A) {
               const int p = pr[e];
               pc[e] = (on && !is_v) ? a.rope_cos[(size_t)p * half + ip] : 0.f;
               ps[e] = (on && !is_v) ? a.rope_sin[(size_t)p * half + ip] : 0.f;
-              pr[e] = (on && n >= a.n_q) ? a.block_table[(size_t)a.slot[t] * a.bt_ld + p / a.page] * a.page + p % a.page
-                                         : 0;
+              // page / row of the token's KV slot (page is a power of two: a shift and a mask,
+              // not two integer divisions per token on the tail's critical path)
+              pr[e] = (on && n >= a.n_q) ? a.block_table[(size_t)a.slot[t] * a.bt_ld + (p >> a.page_shift)] : 0;
+              prow[e] = p & (a.page - 1);
             }
           }
   #pragma unroll
@@ -974,7 +976,7 @@ __device__ __forceinline__ void linear_body(const LinearArgs* __restrict__ A) {
                 if (n < a.n_q) {
                   a.out[(size_t)t * a.ldo + n] = val;
                 } else {
-                  const int pg = pr[e] / a.page, row = pr[e] - pg * a.page;
+                  const int pg = pr[e], row = prow[e];
                   const size_t off = (((size_t)pg * a.n_kv_heads + head) * a.page + row) * a.hd + d;
                   (is_v ? a.vcache : a.kcache)[off] = val;
                 }

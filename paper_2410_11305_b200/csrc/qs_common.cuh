@@ -148,7 +148,7 @@ struct LinearArgs {
   float* kcache;
   float* vcache;
   const int* block_table;
-  int bt_ld, page;
+  int bt_ld, page, page_shift;  // page = 1 << page_shift
   // kOpLogits
   float* arg_val;
   int* arg_idx;

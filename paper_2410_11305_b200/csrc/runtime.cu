@@ -620,6 +620,7 @@ int forward_impl(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const q
     ~RotReset() { g_rotate = 0; }
   } rot_reset;  // the standalone linear API never rotates
   if (m->hadamard && m->group_size != 128) return QS_ERR_CONFIG;
+  if (m->page < 1 || (m->page & (m->page - 1)) != 0) return QS_ERR_CONFIG;  // KV page: a power of two
   // tensor parallel: o_proj / down_proj are row-split, so their outputs are partial
   // sums -> store into ws->attn, all-reduce (caller's hook, e.g. NCCL on this
   // stream), then add into the residual stream
@@ -701,6 +702,7 @@ int forward_impl(const qs_model_t* m, const qs_batch_t* b, int32_t mode, const q
     a.block_table = m->block_table;
     a.bt_ld = m->bt_ld;
     a.page = m->page;
+    a.page_shift = __builtin_ctz((unsigned)m->page);
     return a;
   };
   const qs_tp_t* tp2 = tp ? tp->tp2 : nullptr;

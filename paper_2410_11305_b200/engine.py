@@ -73,7 +73,6 @@ class DecodeEngine:
         hpk = cfg.n_heads // cfg.n_kv_heads
         if G1 * hpk > 64:
             raise ConfigError("gamma+1 query rows per kv head exceed the attention block limit (64)")
-        self._blk = {}
         self.draft_batches = self._batches(1)
         self.verify_batches = self._batches(G1)
         self.use_graphs = use_graphs
@@ -107,18 +106,16 @@ class DecodeEngine:
     def _batches(self, per_seq: int, ctx_cap: int | None = None) -> list[tuple[_lib.Batch, int]]:
         """qs_batch_t descriptors: sequences grouped so each forward has <= 64 tokens.
         ``ctx_cap`` bounds every query's context (pos + 1) in the batch (default: the KV capacity)."""
-        import torch
         seqs_per = max(1, 64 // per_seq)
         out = []
         for s0 in range(0, self.B, seqs_per):
             ns = min(seqs_per, self.B - s0)
-            tok0 = torch.tensor([i * per_seq for i in range(ns)], dtype=torch.int32, device="cuda")
-            ntok = torch.full((ns,), per_seq, dtype=torch.int32, device="cuda")
-            self._blk[(per_seq, s0)] = (tok0, ntok)
             off = s0 * per_seq * 4
+            # uniform blocks (blk_tok0 = NULL): sequence i of the forward = tokens
+            # [i * per_seq, (i + 1) * per_seq) -- the attention skips a block-table load
             b = _lib.Batch(T=ns * per_seq, tokens=self.t["tok"].data_ptr() + off,
                            positions=self.t["pos"].data_ptr() + off, slots=self.t["slot"].data_ptr() + off,
-                           n_blk=ns, blk_tok0=tok0.data_ptr(), blk_ntok=ntok.data_ptr(), blk_qmax=per_seq,
+                           n_blk=ns, blk_tok0=None, blk_ntok=None, blk_qmax=per_seq,
                            ctx_cap=self.kv.capacity if ctx_cap is None else ctx_cap)
             out.append((b, off))
         return out

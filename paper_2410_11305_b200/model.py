@@ -248,6 +248,8 @@ class KVCache:
         import torch
         if gamma_max < 1:
             raise ConfigError("gamma_max must be >= 1")
+        if page < 1 or page & (page - 1):
+            raise ConfigError("KV page size must be a power of two")
         _lib.require_cuda()
         self.config = config
         self.gamma_max = gamma_max

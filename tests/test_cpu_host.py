@@ -63,7 +63,7 @@ def test_workspace_sizes_7b():
     # two operand slots (the fused next-operand emits double-buffer the image), ascale +
     # acorr per slot, per-tile counters + emit counters + emit leaf sums
     assert s.img == 2 * 86 * 192 * 128 and s.ascale == 2 * 86 * 64 * 4 * 5
-    assert s.counters == (4096 + 8 + 1024 + 64 * 128) * 4
+    assert s.counters == (4096 + 8 + 1024 + 2 * 64 * 128) * 4  # + two emit leaf buffers
 
 
 def test_model_config_validation_mirrors_reference():
