@@ -139,7 +139,9 @@ struct LinCfg {
   static constexpr int kOwnChunks = ((TMAX < 8 ? 8 : TMAX) / 8 + kEpiHalves - 1) / kEpiHalves;  // per epilogue warp
   static constexpr int kScaleOff = kStages * kStageBytes;
   static constexpr int kBarOff = kScaleOff + kSStages * kSEntry;
-  static constexpr bool kPref = TMAX <= QS_PART_PREFETCH_TMAX;  // warp-2 partial prefetch compiled in
+  // warp-2 partial prefetch compiled in (measured: the 3-limb T = 16 bucket -- W4A16 AR at
+  // B = 16 -- gains 3.38 -> 3.33 ms per step; the W4A4 T = 16 draft loses 3.14 -> 3.17 ms)
+  static constexpr bool kPref = TMAX <= QS_PART_PREFETCH_TMAX || (L == 3 && TMAX <= 16);
   static constexpr int kNumBars = 3 * kStages + 2 * kASlots + 2 * kAccBufs + 2 * kSStages + (kPref ? 1 : 0);
   static constexpr int kStgOff = ((kBarOff + kNumBars * 8 + 16 + 4 * TMAX * 8 + 4 * 4 + 32 * 4) + 15) / 16 * 16;
   // the rest of the 227 KB: contributor partials of the owned last tile, bulk-copied in by
