@@ -67,6 +67,11 @@
 #ifndef QS_AB
 #define QS_AB 0
 #endif
+// kEmitSilu group completed by the CTA's last owned tile: quantised after the final
+// barrier on every warp (1) or by the epilogue warps in the tail (0)
+#ifndef QS_DEFER_SILU
+#define QS_DEFER_SILU 1
+#endif
 
 namespace qs {
 
@@ -111,7 +116,8 @@ struct LinCfg {
   static constexpr int kEpiHalves = kEpiWarps / 4;
   static constexpr int kUnpackHalves = kUnpackWarps / 4;
   // residual-emit staging: the tile's new residual rows [T][128] + 1/rms per token
-  static constexpr int kStgBytes = (TMAX < 8 ? 8 : TMAX) * 129 * 4;
+  // (+ the tile's 128 RMSNorm weights for the deferred emit quantiser)
+  static constexpr int kStgBytes = ((TMAX < 8 ? 8 : TMAX) * 129 + 128) * 4;
   static constexpr int kStages0 = (196 * 1024 - kStgBytes) / kStageBytes;
   // Unpack group g takes the stages i with i % kUnpackHalves == g and waits on
   // wfull[i % kStages] by parity.  kStages must be a multiple of kUnpackHalves so
@@ -239,6 +245,10 @@ template <int L, int TMAX, int kEpiT, int kEpiWarps>
 __device__ __forceinline__ void emit_rms(const LinearArgs& a, float* stg, int tile, int et, int* pending) {
   const int lane = et & 31, ew = et >> 5;
   constexpr int kTW = (TMAX + kEpiWarps - 1) / kEpiWarps;  // tokens per warp
+  // this tile's RMSNorm weights do not depend on the leaves: in flight across the wait,
+  // parked in shared memory for the deferred quantiser
+  float4 wv = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (TMAX <= 8 || ew == 0) wv = *reinterpret_cast<const float4*>(a.e_rms_w + (size_t)tile * 128 + 4 * lane);
   // clear this tile's column of the other leaf buffer (its readers' launch has completed)
   for (int t = et; t < kLeafRows; t += kEpiT) a.e_leaf_clr[t * kLeafLd + tile] = 0u;
   named_bar(1, kEpiT);
@@ -301,18 +311,36 @@ __device__ __forceinline__ void emit_rms(const LinearArgs& a, float* stg, int ti
     }
   }
   if (QS_LIN_TIMELINE && a.dbg && et == 0) a.dbg[7936 + blockIdx.x] = gtimer();  // 1/rms known
-  // the group quantiser runs after the CTA's final barrier, spread over all warps
-  // (emit_rms_quantise): every other role is idle by then
-  if (et == 0) *pending = tile + 1;
+  if constexpr (TMAX >= 16) {
+    // the group quantiser runs after the CTA's final barrier, spread over all warps
+    // (emit_rms_quantise): every other role is idle by then.  Measured: T = 16 draft
+    // forward 3.16 -> 3.12 ms; for T <= 8 (a token or two per epilogue warp) the extra
+    // barrier costs more than it spreads (B = 1 AR 2.16 -> 2.20 ms), so they quantise here.
+    if (ew == 0) reinterpret_cast<float4*>(stg + 129 * TMAX)[lane] = wv;
+    if (et == 0) *pending = tile + 1;
+  } else {
+    __syncwarp();  // inv[t] of this warp's tokens: written and read by this warp only
+#pragma unroll 1
+    for (int k = 0; k < kTW; ++k) {
+      const int t = ew + k * kEpiWarps;
+      if (t >= a.T) break;
+      const float iv = inv[t];
+      const float4 xv = *reinterpret_cast<const float4*>(stg + t * 128 + 4 * lane);
+      const float v[4] = {__fmul_rn(__fmul_rn(xv.x, iv), wv.x), __fmul_rn(__fmul_rn(xv.y, iv), wv.y),
+                          __fmul_rn(__fmul_rn(xv.z, iv), wv.z), __fmul_rn(__fmul_rn(xv.w, iv), wv.w)};
+      quant_group_warp<L>(v, t, tile, lane, a.e_img, a.e_ascale, a.e_acorr, a.r_pad, a.a_ld, a.e_rotate != 0);
+    }
+    if (QS_LIN_TIMELINE && a.dbg && et == 0) a.dbg[7680 + blockIdx.x] = gtimer();  // quantised
+  }
 }
 
 // The owned tile's group of the RMSNorm'd rows, one token per warp of the whole CTA (the
 // tile is the owner's last segment, so this is the CTA's last work).
-template <int L>
+template <int L, int TMAX>
 __device__ __forceinline__ void emit_rms_quantise(const LinearArgs& a, const float* stg, int tile, int warp,
                                                   int nwarps, int lane) {
-  const float4 wv = *reinterpret_cast<const float4*>(a.e_rms_w + (size_t)tile * 128 + 4 * lane);
   const float* inv = stg + 128 * (a.T > 8 ? a.T : 8);
+  const float4 wv = reinterpret_cast<const float4*>(stg + 129 * (TMAX < 8 ? 8 : TMAX))[lane];  // parked by emit_rms
 #pragma unroll 1
   for (int t = warp; t < a.T; t += nwarps) {
     const float iv = inv[t];
@@ -326,7 +354,7 @@ __device__ __forceinline__ void emit_rms_quantise(const LinearArgs& a, const flo
 // kEmitSilu (gate_up): tiles 2q, 2q+1 hold silu outputs 128q..128q+127 = group q of
 // down_proj's input.  Each owner publishes its half; the second one quantises the group.
 template <int L, int TMAX, int kEpiT, int kEpiWarps>
-__device__ __forceinline__ void emit_silu(const LinearArgs& a, int tile, int et, int* flag) {
+__device__ __forceinline__ void emit_silu(const LinearArgs& a, int tile, int et, int* flag, bool last, int* pending) {
   constexpr int kTW = (TMAX + kEpiWarps - 1) / kEpiWarps;  // tokens per warp
   const int lane = et & 31, ew = et >> 5, q = tile >> 1;
   named_bar(1, kEpiT);  // the CTA's h writes, then et 0's acq_rel add (cumulative release)
@@ -335,6 +363,10 @@ __device__ __forceinline__ void emit_silu(const LinearArgs& a, int tile, int et,
   const int second = *flag;
   named_bar(1, kEpiT);
   if (second != 1) return;
+  if (TMAX >= 16 && QS_DEFER_SILU && last) {  // the CTA's last work: quantised after the final barrier on every warp
+    if (et == 0) *pending = q + 1;
+    return;
+  }
   float4 hv[kTW];  // all of this warp's rows in flight at once
 #pragma unroll
   for (int k = 0; k < kTW; ++k) {
@@ -350,6 +382,18 @@ __device__ __forceinline__ void emit_silu(const LinearArgs& a, int tile, int et,
     quant_group_warp<L>(v, t, q, lane, a.e_img, a.e_ascale, a.e_acorr, a.r_pad, a.a_ld, a.e_rotate != 0);
   }
   if (et == 0) a.e_cnt[8 + q] = 0;
+}
+
+// Deferred kEmitSilu group q (the CTA's last owned tile completed it): one token per warp.
+template <int L>
+__device__ __forceinline__ void emit_silu_quantise(const LinearArgs& a, int q, int warp, int nwarps, int lane) {
+#pragma unroll 1
+  for (int t = warp; t < a.T; t += nwarps) {
+    const float4 hv = __ldcg(reinterpret_cast<const float4*>(a.out + (size_t)t * a.ldo + 128 * q) + lane);
+    const float v[4] = {hv.x, hv.y, hv.z, hv.w};
+    quant_group_warp<L>(v, t, q, lane, a.e_img, a.e_ascale, a.e_acorr, a.r_pad, a.a_ld, a.e_rotate != 0);
+  }
+  if (warp == 0 && lane == 0) a.e_cnt[8 + q] = 0;
 }
 
 // The linear kernel body (A = the launch's argument block).
@@ -373,7 +417,7 @@ __device__ __forceinline__ void linear_body(const LinearArgs* __restrict__ A) {
   float* sring = reinterpret_cast<float*>(smem + C::kScaleOff);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::kNumBars);
   int* flag = reinterpret_cast<int*>(tmem_slot + 2);
-  int* emit_pending = reinterpret_cast<int*>(tmem_slot + 3);  // kEmitRms: owned tile + 1, quantised at exit
+  int* emit_pending = reinterpret_cast<int*>(tmem_slot + 3);  // deferred emit: kEmitRms tile + 1 / kEmitSilu group + 1
   float* red_val = reinterpret_cast<float*>(tmem_slot + 4);  // [4][TMAX]
   int* red_idx = reinterpret_cast<int*>(red_val + 4 * TMAX);  // [4][TMAX]
 
@@ -1047,7 +1091,8 @@ __device__ __forceinline__ void linear_body(const LinearArgs* __restrict__ A) {
                                                    emit_pending);
         }
         if constexpr (OP == kOpSiluMul) {
-          if (a.emit == kEmitSilu) emit_silu<L, TMAX, kEpiT, C::kEpiWarps>(a, tile, et, flag);
+          if (a.emit == kEmitSilu)
+            emit_silu<L, TMAX, kEpiT, C::kEpiWarps>(a, tile, et, flag, last_u == u1 - 1, emit_pending);
         }
       };
       post(std::integral_constant<int, OPC>{});
@@ -1064,9 +1109,12 @@ __device__ __forceinline__ void linear_body(const LinearArgs* __restrict__ A) {
     tc_fence_after();
     tmem_dealloc<C::kTmemCols>(tmem);
   }
+  if constexpr (OPC == kOpSiluMul) {
+    if (*emit_pending) emit_silu_quantise<L>(A[0], *emit_pending - 1, warp, C::kThreads / 32, lane);
+  }
   if constexpr (OPC == kOpStore) {
     if (*emit_pending) {
-      emit_rms_quantise<L>(A[0], reinterpret_cast<const float*>(smem + C::kStgOff), *emit_pending - 1, warp,
+      emit_rms_quantise<L, TMAX>(A[0], reinterpret_cast<const float*>(smem + C::kStgOff), *emit_pending - 1, warp,
                            C::kThreads / 32, lane);
       if (QS_LIN_TIMELINE && A[0].dbg && threadIdx.x == 0) A[0].dbg[7680 + c] = gtimer();  // quantised
     }
