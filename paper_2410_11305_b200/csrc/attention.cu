@@ -25,8 +25,8 @@ constexpr int kAttnChunk = QS_ATTN_CHUNK;
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) { cp_async16_cg(smem, gmem); }
 
 // Scores of keys jj = warp + 8u (u < KPW) for every query, QB queries at a time:
-// per (key, query) a lane-ordered fma chain then p += shfl_xor(p, 16..1); the
-// independent pairs' trees are interleaved.
+// per (key, query) a lane-ordered fma chain, then the xor-butterfly total of the lanes'
+// partials (computed by recursive halving, see below).
 template <int QB, int KPW>
 __device__ __forceinline__ void score_block(const float* kt, const float* qv, float* sc, const int* ctx_s, int hd,
                                             int Q, int nk, int j0, int warp, int lane, float inv_sqrt_hd) {
@@ -52,22 +52,38 @@ __device__ __forceinline__ void score_block(const float* kt, const float* qv, fl
         }
       }
     }
+    // Reduce the NP = KPW * QB (key, query) partials across the lanes.  The reference
+    // arithmetic is the xor butterfly p += shfl_xor(p, 16), 8, 4, 2, 1 (every lane ends
+    // with every pair's total); here the levels with offset >= NP stay butterflies and the
+    // rest are recursive halving -- at offset o a lane keeps the half of its pairs selected
+    // by its lane bit o and adds the partner's value of the same pair, which is exactly the
+    // butterfly's v_l + v_(l^o) for the pairs it keeps.  Lane l ends with pair l % NP:
+    // bit-identical totals for ~31 shuffles per lane instead of 5 * NP.
+    constexpr int NP = KPW * QB;
+    static_assert((NP & (NP - 1)) == 0 && NP <= 32, "pairs per warp: a power of two <= 32");
+    float v[NP];
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1)
+    for (int u = 0; u < KPW; ++u)
 #pragma unroll
-      for (int u = 0; u < KPW; ++u)
+      for (int qq = 0; qq < QB; ++qq) v[u * QB + qq] = p[u][qq];
 #pragma unroll
-        for (int qq = 0; qq < QB; ++qq) p[u][qq] += __shfl_xor_sync(0xffffffffu, p[u][qq], off);
-    if (lane == 0) {
+    for (int off = 16; off >= NP; off >>= 1)
 #pragma unroll
-      for (int u = 0; u < KPW; ++u) {
-        const int jj = warp + 8 * u, j = j0 + jj;
+      for (int i = 0; i < NP; ++i) v[i] += __shfl_xor_sync(0xffffffffu, v[i], off);
 #pragma unroll
-        for (int qq = 0; qq < QB; ++qq) {
-          const int qi = q0 + qq;
-          if (jj < nk && qi < Q) sc[qi * kAttnChunk + jj] = (j < ctx_s[qi]) ? p[u][qq] * inv_sqrt_hd : -INFINITY;
-        }
+    for (int n = NP; n > 1; n >>= 1) {
+      const int h = n >> 1;
+      const bool hi = (lane & h) != 0;
+#pragma unroll
+      for (int i = 0; i < h; ++i) {
+        const float keep = hi ? v[i + h] : v[i], send = hi ? v[i] : v[i + h];
+        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, h);
       }
+    }
+    if (lane < NP) {
+      const int u = lane / QB, qq = lane % QB;
+      const int jj = warp + 8 * u, j = j0 + jj, qi = q0 + qq;
+      if (jj < nk && qi < Q) sc[qi * kAttnChunk + jj] = (j < ctx_s[qi]) ? v[0] * inv_sqrt_hd : -INFINITY;
     }
   }
 }
@@ -192,15 +208,71 @@ __global__ void __launch_bounds__(256) attn_partial_kernel(const AttnArgs a) {
   }
   __syncthreads();
 
-  // ---- o_c = sum_j p_j v_j  (thread per (query, dim))
+  // ---- o_c = sum_j p_j v_j: per (query, dim) one sequential fma chain over the chunk's
+  // keys.  Thread (g, d) owns dim d of queries g, g + G, ... (G = 256 / hd), four at a
+  // time, so each V element is read once per four queries and the probabilities four keys
+  // per 16-byte load; the chains themselves are unchanged.
   mbar_wait(&kv_bar[1], 0);
-  for (int e = tid; e < Q * hd; e += blockDim.x) {
-    const int qi = hs >= 0 ? e >> hs : e / hd, d = e - qi * hd;
-    const float* p = sc + qi * kAttnChunk;
-    float acc = 0.f;
-    for (int jj = 0; jj < nk; ++jj) acc = fmaf(p[jj], vt[jj * hd + d], acc);
-    const int i = qi / hpk, h = kvh * hpk + qi % hpk;
-    a.part_o[(((size_t)(tok0 + i) * H + h) * a.cmax + ch) * hd + d] = acc;
+  if (hd <= (int)blockDim.x && blockDim.x % hd == 0) {
+    const int G = blockDim.x / hd, g = tid / hd, d = tid - g * hd;
+    if (Q <= G) {  // one query per thread (decode steps): a single chain
+      if (g < Q) {
+        const float* pq = sc + g * kAttnChunk;
+        float acc = 0.f;
+        int jj = 0;
+        for (; jj + 4 <= nk; jj += 4) {
+          const float4 pp = *reinterpret_cast<const float4*>(pq + jj);
+          acc = fmaf(pp.x, vt[jj * hd + d], acc);
+          acc = fmaf(pp.y, vt[(jj + 1) * hd + d], acc);
+          acc = fmaf(pp.z, vt[(jj + 2) * hd + d], acc);
+          acc = fmaf(pp.w, vt[(jj + 3) * hd + d], acc);
+        }
+        for (; jj < nk; ++jj) acc = fmaf(pq[jj], vt[jj * hd + d], acc);
+        const int i = g / hpk, h = kvh * hpk + g % hpk;
+        a.part_o[(((size_t)(tok0 + i) * H + h) * a.cmax + ch) * hd + d] = acc;
+      }
+    } else
+    for (int q0 = g; q0 < Q; q0 += 4 * G) {
+      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+      const float* pr[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) pr[u] = sc + min(q0 + u * G, Q - 1) * kAttnChunk;
+      int jj = 0;
+      for (; jj + 4 <= nk; jj += 4) {
+        const float v0 = vt[jj * hd + d], v1 = vt[(jj + 1) * hd + d], v2 = vt[(jj + 2) * hd + d],
+                    v3 = vt[(jj + 3) * hd + d];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const float4 pp = *reinterpret_cast<const float4*>(pr[u] + jj);
+          acc[u] = fmaf(pp.x, v0, acc[u]);
+          acc[u] = fmaf(pp.y, v1, acc[u]);
+          acc[u] = fmaf(pp.z, v2, acc[u]);
+          acc[u] = fmaf(pp.w, v3, acc[u]);
+        }
+      }
+      for (; jj < nk; ++jj) {
+        const float vj = vt[jj * hd + d];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) acc[u] = fmaf(pr[u][jj], vj, acc[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int qi = q0 + u * G;
+        if (qi < Q) {
+          const int i = qi / hpk, h = kvh * hpk + qi % hpk;
+          a.part_o[(((size_t)(tok0 + i) * H + h) * a.cmax + ch) * hd + d] = acc[u];
+        }
+      }
+    }
+  } else {
+    for (int e = tid; e < Q * hd; e += blockDim.x) {
+      const int qi = hs >= 0 ? e >> hs : e / hd, d = e - qi * hd;
+      const float* p = sc + qi * kAttnChunk;
+      float acc = 0.f;
+      for (int jj = 0; jj < nk; ++jj) acc = fmaf(p[jj], vt[jj * hd + d], acc);
+      const int i = qi / hpk, h = kvh * hpk + qi % hpk;
+      a.part_o[(((size_t)(tok0 + i) * H + h) * a.cmax + ch) * hd + d] = acc;
+    }
   }
 }
 
