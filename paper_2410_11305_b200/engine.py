@@ -86,7 +86,7 @@ class DecodeEngine:
         # this bound instead of the KV capacity drops the CTAs past every sequence's context
         # (at prompt 128, capacity 520: 9 chunk slots per (block, kv head), 3 in use).
         self._ctx_hi = 0
-        self._page = _lib.load().qs_attention_chunk_len()
+        self._chunk = _lib.load().qs_attention_chunk_len()   # keys per split-KV chunk
 
     def _setup_storage(self, model: TransformerModel, batch: int, gamma: int) -> None:
         """KV pool, workspace and the C model view the forwards run on (TP overrides)."""
@@ -160,7 +160,7 @@ class DecodeEngine:
         """Attention context bound of a step starting at max(committed) <= ctx_hi, rounded
         up to whole key chunks (one captured graph per chunk count)."""
         need = ctx_hi + self._advance()   # positions committed .. committed + gamma
-        c = self._page
+        c = self._chunk
         return min(self.kv.capacity, -(-need // c) * c)
 
     def _set_ctx_cap(self, cap: int) -> None:
