@@ -69,6 +69,9 @@
 #endif
 // kEmitSilu group completed by the CTA's last owned tile: quantised after the final
 // barrier on every warp (1) or by the epilogue warps in the tail (0)
+#ifndef QS_CORR_MMA
+#define QS_CORR_MMA 1
+#endif
 #ifndef QS_DEFER_SILU
 #define QS_DEFER_SILU 1
 #endif
@@ -91,15 +94,27 @@ struct LinCfg {
   // hands the buffer back right after its tcgen05.ld
   static constexpr bool kOneAcc = QS_ONE_ACC && kCPS0 == 1 && (2 * kAccCols + 2 * 2 * 32 <= 512);
   static constexpr int kCPS = kOneAcc ? 2 : kCPS0;
+  // Offset-binary correction on the tensor core (small-token buckets, kUns below): after a
+  // chunk's four K-steps, four more MMAs with a constant A of -8 bytes (8 TMEM columns,
+  // written once) add -8 * sum_k x to every row, so D is the signed dot product and the
+  // epilogue neither loads nor subtracts the per-(chunk, token) sums.  Measured: the
+  // 3-limb T = 16 bucket gains (W4A16 AR B=16 3.31 -> 3.24 ms per step); the W4A4 T = 16
+  // draft is neutral and the T <= 8 buckets lose (B=1 AR 2.13 -> 2.16 ms: the shallower
+  // A ring and the extra MMA issue sit on their latency-bound stages), so only there.
+  static constexpr bool kUns0 = TMAX <= 16;
+  static constexpr bool kCorrMma = QS_CORR_MMA && L == 3 && TMAX == 16 &&
+                                   ((kOneAcc ? 1 : 2) * kCPS * kAccCols + 2 * kCPS * 32 + 32 <= 512);
+  static constexpr int kConstCols = kCorrMma ? 32 : 0;
   // spend leftover TMEM on deeper rings (lets unpack / epilogue run further ahead)
-  static constexpr int kFree0 = 512 - (kOneAcc ? 1 : 2) * kCPS * kAccCols - 2 * kCPS * 32;
+  static constexpr int kFree0 = 512 - (kOneAcc ? 1 : 2) * kCPS * kAccCols - 2 * kCPS * 32 - kConstCols;
   static constexpr int kASlots = 2 + (kFree0 >= kCPS * 32 ? 1 : 0);
   static constexpr int kFree1 = kFree0 - (kASlots - 2) * kCPS * 32;
   static constexpr int kAccBufs =
       kOneAcc ? 1 : 2 + (kFree1 / (kCPS * kAccCols) > 2 ? 2 : kFree1 / (kCPS * kAccCols));
   static constexpr int kAColBase = kAccBufs * kCPS * kAccCols;
+  static constexpr int kAConst = kAColBase + kASlots * kCPS * 32;  // constant -8 A columns (kCorrMma)
   static constexpr int kTmemCols = 512;
-  static_assert(kAColBase + kASlots * kCPS * 32 <= kTmemCols, "TMEM budget");
+  static_assert(kAConst + kConstCols <= kTmemCols, "TMEM budget");
   static constexpr int kActBytes = kRowsMax * 128;
   static constexpr int kStageBytes = kCPS * (kChunkBytes + kActBytes);
   // 16 warps: 4 control, then unpack and epilogue warps (2 or 1 per TMEM lane
@@ -134,7 +149,7 @@ struct LinCfg {
   // and subtract 8 * sum(x) per (chunk, token, limb) in the epilogue; buckets with
   // T >= 32 are epilogue-bound, so they convert to signed bytes in the unpack instead
   // (measured: the correction cost T=64 draft 79 -> 89 us on 28672x8192).
-  static constexpr bool kUns = TMAX <= 16;
+  static constexpr bool kUns = kUns0;
   static constexpr int kALd = TMAX < 8 ? 8 : TMAX;  // ascale rows are a_ld = roundup(T, 8) <= kALd
   // scale ring entry: [kCPS][128] weight scales | [kCPS][a_ld] activation scales | (kUns)
   // [kCPS][a_ld][4] correction sums
@@ -573,10 +588,10 @@ __device__ __forceinline__ void linear_body(const LinearArgs* __restrict__ A) {
     {
       QS_LIN_GEOM(0)
       const uint32_t a_bytes = (uint32_t)a.a_ld * 4u;
-      const uint32_t e_bytes = 512u + (C::kUns ? 5u : 1u) * a_bytes;  // per chunk
+      const uint32_t e_bytes = 512u + ((C::kUns && !C::kCorrMma) ? 5u : 1u) * a_bytes;  // per chunk
       auto act_part = [&](float* se, const StageIt& st, int ss) {
         bulk_g2s_elect(se + CPS * 128, a.ascale + (size_t)st.ch0 * a.a_ld, st.nq * a_bytes, &sfull[ss]);
-        if (C::kUns)
+        if (C::kUns && !C::kCorrMma)
           bulk_g2s_elect(se + C::kCorrOff, a.acorr + (size_t)st.ch0 * a.a_ld * 4, st.nq * 4u * a_bytes, &sfull[ss]);
       };
       StageIt it{u0, u1, NC, CPS};
@@ -632,6 +647,7 @@ __device__ __forceinline__ void linear_body(const LinearArgs* __restrict__ A) {
     {
       QS_LIN_GEOM(0)
       const uint32_t idesc = idesc_i8(128, (uint32_t)a.r_pad, !C::kUns);
+      const uint32_t idesc_s = idesc_i8(128, (uint32_t)a.r_pad, true);  // the constant -8 A is signed
       StageIt it{u0, u1, NC, CPS};
       for (; it.next(); ++i) {
         const int s = i % C::kStages, b = i % C::kAccBufs, as_ = i % C::kASlots;
@@ -651,9 +667,13 @@ __device__ __forceinline__ void linear_body(const LinearArgs* __restrict__ A) {
         const uint32_t a0 = tmem + C::kAColBase + as_ * CPS * 32;
 #pragma unroll
         for (int q = 0; q < CPS; ++q)
-          if (!(QS_AB & 2) && q < it.nq)
+          if (!(QS_AB & 2) && q < it.nq) {
             mma_i8_ts_chunk4_elect(d0 + q * C::kAccCols, a0 + q * 32,
                                    bdesc0 + (uint64_t)((q * C::kActBytes) >> 4), idesc);
+            if constexpr (C::kCorrMma)
+              mma_i8_ts_const4_elect(d0 + q * C::kAccCols, tmem + C::kAConst,
+                                     bdesc0 + (uint64_t)((q * C::kActBytes) >> 4), idesc_s);
+          }
         if (dbg0 && i < 64 && lane == 0) a.dbg[8 * 64 + i] = gtimer();
         mma_commit_elect(&empty[s]);
         mma_commit_elect(&tempty[as_]);
@@ -668,6 +688,13 @@ __device__ __forceinline__ void linear_body(const LinearArgs* __restrict__ A) {
     // latency chains (LDS -> ALU -> tcgen05.st -> wait) overlap.
     const int q4 = warp & 3, ug = (warp - 4) >> 2, r = q4 * 32 + lane;
     const uint32_t lane_base = (uint32_t)(q4 * 32) << 16;
+    if (C::kCorrMma && ug == 0) {
+      // the constant -8 A operand: waited for (tcgen05.wait::st) with the group's first
+      // stage, which the MMA issuer waits for before any MMA reads it
+      const uint32_t m8[8] = {0xF8F8F8F8u, 0xF8F8F8F8u, 0xF8F8F8F8u, 0xF8F8F8F8u,
+                              0xF8F8F8F8u, 0xF8F8F8F8u, 0xF8F8F8F8u, 0xF8F8F8F8u};
+      tmem_st8(tmem + lane_base + C::kAConst, m8);
+    }
     int i = 0;
     {
     QS_LIN_GEOM(0)
@@ -766,7 +793,8 @@ __device__ __forceinline__ void linear_body(const LinearArgs* __restrict__ A) {
               tmem_wait_ld();
               for (int e = 0; e < 8; ++e) {
                 const int col = c0 + e, tt = col / L, l = col - tt * L;
-                const int32_t corr = (C::kUns && tt < a.T) ? a.acorr[((size_t)ch * a.a_ld + tt) * 4 + l] : 0;
+                const int32_t corr =
+                    (C::kUns && !C::kCorrMma && tt < a.T) ? a.acorr[((size_t)ch * a.a_ld + tt) * 4 + l] : 0;
                 a.dump[((size_t)n * NC + ch) * a.r_pad + col] = (int32_t)rr[e] - corr;
               }
             }
@@ -844,13 +872,13 @@ __device__ __forceinline__ void linear_body(const LinearArgs* __restrict__ A) {
                 for (int u = 0; u < 2; ++u) {
                   // offset-binary correction (kUns): D = D' - 8 * S per limb
                   if constexpr (L == 1) {
-                    const int c0 = C::kUns ? corr[4 * (e + u)] : 0;
+                    const int c0 = (C::kUns && !C::kCorrMma) ? corr[4 * (e + u)] : 0;
                     dv[u] = (float)((int32_t)rr[q][e + u] - c0);
                   } else {
                     // token-major, limb-minor columns: X = l2*2^16 + l1*2^8 + l0.
                     // d1*256+d0 is exact in int32; one rounding in the fma.
-                    const int2 cr =
-                        C::kUns ? *reinterpret_cast<const int2*>(corr + 4 * (e + u) + 2) : make_int2(0, 0);
+                    const int2 cr = (C::kUns && !C::kCorrMma) ? *reinterpret_cast<const int2*>(corr + 4 * (e + u) + 2)
+                                                              : make_int2(0, 0);
                     const int32_t lo = (int32_t)rr[q][3 * (e + u) + 1] * 256 + (int32_t)rr[q][3 * (e + u)] - cr.y;
                     dv[u] = (float)lo;
                     rr[q][3 * (e + u) + 2] = __float_as_uint((float)((int32_t)rr[q][3 * (e + u) + 2] - cr.x));
@@ -869,12 +897,13 @@ __device__ __forceinline__ void linear_body(const LinearArgs* __restrict__ A) {
                 float dv;
                 // offset-binary correction (kUns): D = D' - 8 * S per limb
                 if constexpr (L == 1) {
-                  const int c0 = C::kUns ? corr[4 * e] : 0;
+                  const int c0 = (C::kUns && !C::kCorrMma) ? corr[4 * e] : 0;
                   dv = (float)((int32_t)rr[q][e] - c0);
                 } else {
                   // token-major, limb-minor columns: X = l2*2^16 + l1*2^8 + l0.
                   // d1*256+d0 is exact in int32; one rounding in the fma.
-                  const int2 cr = C::kUns ? *reinterpret_cast<const int2*>(corr + 4 * e + 2) : make_int2(0, 0);
+                  const int2 cr = (C::kUns && !C::kCorrMma) ? *reinterpret_cast<const int2*>(corr + 4 * e + 2)
+                                                            : make_int2(0, 0);
                   const int32_t lo = (int32_t)rr[q][3 * e + 1] * 256 + (int32_t)rr[q][3 * e] - cr.y;
                   dv = fmaf((float)((int32_t)rr[q][3 * e + 2] - cr.x), 65536.0f, (float)lo);
                 }

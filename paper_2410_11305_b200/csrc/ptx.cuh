@@ -225,6 +225,23 @@ __device__ __forceinline__ void mma_i8_ts_chunk4_elect(uint32_t d_tmem, uint32_t
       : "memory");
 }
 
+// Four accumulating K=32 MMAs with one constant A block (8 TMEM columns reused for every
+// K step) against the chunk's four B slices: D += A_const . B over the 128-wide chunk.
+__device__ __forceinline__ void mma_i8_ts_const4_elect(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
+                                                       uint32_t idesc) {
+  asm volatile(
+      "{\n\t.reg .pred p1, e;\n\t.reg .b64 b1, b2, b3;\n\t"
+      "setp.eq.b32 p1, %0, %0;\n\t"
+      "add.u64 b1, %2, 2;\n\tadd.u64 b2, %2, 4;\n\tadd.u64 b3, %2, 6;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], b1, %3, p1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], b2, %3, p1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], b3, %3, p1;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc)
+      : "memory");
+}
+
 // Same, A from shared memory (used by the self-test of the descriptor path).
 __device__ __forceinline__ void mma_i8_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
                                           uint32_t accumulate) {
