@@ -392,7 +392,6 @@ int qs_workspace_size(const qs_model_t* m, int32_t t_max, qs_workspace_sizes_t* 
   fill_geometry(m->d_model, m->d_ff, m->group_size, &wf);
   fill_geometry(m->vocab, m->d_model, m->group_size, &wl);
   const int chunks = wd.n_chunks > wf.n_chunks ? wd.n_chunks : wf.n_chunks;
-  const int groups = wd.G > wf.G ? wd.G : wf.G;
   int tiles = wl.n_tiles;
   const int t_ff = round_up(2 * m->d_ff, kTileN) / kTileN;
   const int t_qkv = round_up((m->n_heads + 2 * m->n_kv_heads) * hd, kTileN) / kTileN;
