@@ -63,15 +63,18 @@
 
 // research ablations (scripts/lin_ablate.sh), 0 in the product build; bit 0: unpack skips
 // LDS + ALU, 1: no MMAs (commits only), 2: epilogue skips TMEM loads + math, 3: unpack
-// skips tcgen05.st, 4: no weight bulk copies (the ring fills without HBM traffic)
+// skips tcgen05.st, 4: no weight bulk copies (the ring fills without HBM traffic),
+// 5: epilogue keeps its TMEM loads but skips the scale-accumulate math
 #ifndef QS_AB
 #define QS_AB 0
 #endif
-// kEmitSilu group completed by the CTA's last owned tile: quantised after the final
-// barrier on every warp (1) or by the epilogue warps in the tail (0)
+// offset-binary correction by a constant-A MMA where LinCfg::kCorrMma allows (1) or in the
+// epilogue everywhere (0)
 #ifndef QS_CORR_MMA
 #define QS_CORR_MMA 1
 #endif
+// kEmitSilu group completed by the CTA's last owned tile: quantised after the final
+// barrier on every warp (1) or by the epilogue warps in the tail (0)
 #ifndef QS_DEFER_SILU
 #define QS_DEFER_SILU 1
 #endif
@@ -432,7 +435,17 @@ __device__ __forceinline__ void linear_body(const LinearArgs* __restrict__ A) {
   using C = LinCfg<L, TMAX>;
   constexpr int CPS = C::kCPS;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte aligned base.  For T >= 32 as an OFFSET from the shared array: the compiler
+  // keeps the shared address space, so the ring / scale / staging accesses are LDS / STS
+  // (verify forward 6.25 -> 6.09 ms).  The small-token buckets keep the integer round trip
+  // (generic LD / ST): with the address space known the compiler batches more shared loads
+  // ahead, which costs registers (T <= 2: 116 -> 128) and measured slower (B=1 AR 2.13 ->
+  // 2.24 ms, AR B=16 3.22 -> 3.29 ms).
+  uint8_t* smem;
+  if constexpr (TMAX >= 32)
+    smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  else
+    smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kBarOff);
   uint64_t* wfull = bars;                      // [kStages] stage weights landed (tx bytes)
   uint64_t* afull = wfull + C::kStages;        // [kStages] stage activation image landed
@@ -853,7 +866,7 @@ __device__ __forceinline__ void linear_body(const LinearArgs* __restrict__ A) {
           }
 #pragma unroll
           for (int q = 0; q < CPS; ++q) {
-            if (q < it.nq) {
+            if (!(QS_AB & 32) && q < it.nq) {
               const float* asc = se + CPS * 128 + q * a.a_ld;
               const float4 s0 = *reinterpret_cast<const float4*>(asc + tc * 8);
               const float4 s1 = *reinterpret_cast<const float4*>(asc + tc * 8 + 4);
