@@ -457,7 +457,8 @@ __device__ __forceinline__ void linear_body(const LinearArgs* __restrict__ A) {
   uint64_t* sfull = accempty + C::kAccBufs;    // [kSStages] scales landed
   uint64_t* sempty = sfull + C::kSStages;      // [kSStages] epilogue -> scale producer
   uint64_t* pbar = sempty + C::kSStages;       // [1] prefetched contributor partials landed
-  float* sring = reinterpret_cast<float*>(smem + C::kScaleOff);
+  // the scale ring (read by the epilogue every stage) always through the shared space
+  float* sring = reinterpret_cast<float*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u) + C::kScaleOff);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::kNumBars);
   int* flag = reinterpret_cast<int*>(tmem_slot + 2);
   int* emit_pending = reinterpret_cast<int*>(tmem_slot + 3);  // deferred emit: kEmitRms tile + 1 / kEmitSilu group + 1
