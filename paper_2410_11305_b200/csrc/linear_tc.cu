@@ -457,8 +457,10 @@ __device__ __forceinline__ void linear_body(const LinearArgs* __restrict__ A) {
   uint64_t* sfull = accempty + C::kAccBufs;    // [kSStages] scales landed
   uint64_t* sempty = sfull + C::kSStages;      // [kSStages] epilogue -> scale producer
   uint64_t* pbar = sempty + C::kSStages;       // [1] prefetched contributor partials landed
-  // the scale ring (read by the epilogue every stage) always through the shared space
-  float* sring = reinterpret_cast<float*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u) + C::kScaleOff);
+  // the scale ring (read by the epilogue every stage) and the weight ring's unpack loads
+  // always through the shared space
+  uint8_t* const smem_sh = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  float* sring = reinterpret_cast<float*>(smem_sh + C::kScaleOff);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + C::kNumBars);
   int* flag = reinterpret_cast<int*>(tmem_slot + 2);
   int* emit_pending = reinterpret_cast<int*>(tmem_slot + 3);  // deferred emit: kEmitRms tile + 1 / kEmitSilu group + 1
@@ -727,7 +729,7 @@ __device__ __forceinline__ void linear_body(const LinearArgs* __restrict__ A) {
 #pragma unroll
       for (int q = 0; q < kPre; ++q) {
         if (!(QS_AB & 1) && q < it.nq) {
-          const uint4* src = reinterpret_cast<const uint4*>(smem + s * C::kStageBytes + q * kChunkBytes);
+          const uint4* src = reinterpret_cast<const uint4*>(smem_sh + s * C::kStageBytes + q * kChunkBytes);
 #pragma unroll
           for (int jp = 0; jp < 4; ++jp) wv[q][jp] = src[jp * 128 + r];
         }
@@ -736,7 +738,7 @@ __device__ __forceinline__ void linear_body(const LinearArgs* __restrict__ A) {
       for (int q = 0; q < CPS; ++q) {
         if (q < it.nq) {
           if (!(QS_AB & 1) && q >= kPre) {
-            const uint4* src = reinterpret_cast<const uint4*>(smem + s * C::kStageBytes + q * kChunkBytes);
+            const uint4* src = reinterpret_cast<const uint4*>(smem_sh + s * C::kStageBytes + q * kChunkBytes);
 #pragma unroll
             for (int jp = 0; jp < 4; ++jp) wv[q][jp] = src[jp * 128 + r];
           }
