@@ -55,10 +55,11 @@
 #define QS_U8E8_T 0
 #endif
 // warp-2 contributor-partial prefetch for buckets T <= this (others: the owner polls and
-// gathers).  Measured: B=1 AR 2.36 -> 2.34 ms, B=1 QSpec cycle 10.1 -> 9.9 ms; at T = 16 it
-// cost ~1 % (B=16 16.74 -> 16.91 ms per cycle), so the T = 16 bucket keeps the gather.
+// gathers).  Measured: B=1 AR 2.36 -> 2.34 ms, B=1 QSpec cycle 10.1 -> 9.9 ms at T <= 8; at
+// T = 16 it first cost ~1 % (instruction footprint), and after the shared-space addressing
+// of the rings it gains ~0.5 % (B=16 cycle 15.05 -> 15.04, AR B=16 3.21 -> 3.19 ms)
 #ifndef QS_PART_PREFETCH_TMAX
-#define QS_PART_PREFETCH_TMAX 8
+#define QS_PART_PREFETCH_TMAX 16
 #endif
 
 // research ablations (scripts/lin_ablate.sh), 0 in the product build; bit 0: unpack skips
@@ -163,9 +164,7 @@ struct LinCfg {
   static constexpr int kOwnChunks = ((TMAX < 8 ? 8 : TMAX) / 8 + kEpiHalves - 1) / kEpiHalves;  // per epilogue warp
   static constexpr int kScaleOff = kStages * kStageBytes;
   static constexpr int kBarOff = kScaleOff + kSStages * kSEntry;
-  // warp-2 partial prefetch compiled in (measured: the 3-limb T = 16 bucket -- W4A16 AR at
-  // B = 16 -- gains 3.38 -> 3.33 ms per step; the W4A4 T = 16 draft loses 3.14 -> 3.17 ms)
-  static constexpr bool kPref = TMAX <= QS_PART_PREFETCH_TMAX || (L == 3 && TMAX <= 16);
+  static constexpr bool kPref = TMAX <= QS_PART_PREFETCH_TMAX;  // warp-2 partial prefetch compiled in
   static constexpr int kNumBars = 3 * kStages + 2 * kASlots + 2 * kAccBufs + 2 * kSStages + (kPref ? 1 : 0);
   static constexpr int kStgOff = ((kBarOff + kNumBars * 8 + 16 + 4 * TMAX * 8 + 4 * 4 + 32 * 4) + 15) / 16 * 16;
   // the rest of the 227 KB: contributor partials of the owned last tile, bulk-copied in by
