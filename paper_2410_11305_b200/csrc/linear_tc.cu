@@ -436,10 +436,12 @@ __device__ __forceinline__ void linear_body(const LinearArgs* __restrict__ A) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte aligned base.  For T >= 32 as an OFFSET from the shared array: the compiler
   // keeps the shared address space, so the ring / scale / staging accesses are LDS / STS
-  // (verify forward 6.25 -> 6.09 ms).  The small-token buckets keep the integer round trip
-  // (generic LD / ST): with the address space known the compiler batches more shared loads
-  // ahead, which costs registers (T <= 2: 116 -> 128) and measured slower (B=1 AR 2.13 ->
-  // 2.24 ms, AR B=16 3.22 -> 3.29 ms).
+  // (verify forward 6.25 -> 6.09 ms).  The small-token buckets form `smem` through an
+  // integer round trip (generic LD / ST) and address only the scale ring and the unpack's
+  // weight-ring loads through `smem_sh` below: with the whole kernel (or just the owner
+  // tail's staging / partial buffers) in the shared space the compiler batches more shared
+  // loads ahead in the tail, which costs registers (T <= 2: 116 -> 128) and measured slower
+  // (B=1 AR 2.13 -> 2.24 ms, AR B=16 3.22 -> 3.29 ms).
   uint8_t* smem;
   if constexpr (TMAX >= 32)
     smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
